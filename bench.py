@@ -1,0 +1,396 @@
+#!/usr/bin/env python
+"""MSDA forward benchmark on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+One step = one MSDA forward call over one batch (one scene) of the named
+configuration.  Default workload = BASELINE configs[1] ("cfg2"): the
+outside-in warehouse scene, 16 static cameras, 4 levels of 1080p-derived
+features (270x480 .. 33x60, the reference bench generator's floor halving),
+900 anchors x 13 keypoints per level per camera, C=256, fp32, exact
+(bit-faithful) CSR path — inputs byte-identical to the reference's own
+``generate_workload`` (seed = rank; rank 0 is the reference's seed 0).
+
+Multi-GPU (torchrun): stream-sharded — every rank owns an independent scene
+(no data-path collective); ``value`` = all ranks' camera-frames / max-rank
+time.  ``--impl reference`` times the reference's CPU algorithm (the oracle
+port of ``msda_optimized``, all host threads) on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2601_10819_b200.workload import BenchWorkload, generate_workload  # noqa: E402
+
+METRIC = "MSDA fwd camera-streams/sec per B200 (camera-frames/s)"
+CONFIGS = {
+    "cfg2": dict(
+        desc="outside-in warehouse scene: 16 static cams, 4 levels 270x480/135x240/67x120/33x60 (1080p strides "
+             "4-32, reference bench floor halving), 900 anchors, 13 keypoints, C=256, fp32, exact CSR plan",
+        wl=dict(cameras=16, levels=4, channels=256, queries=900, points_per_query=13, level0_size=(270, 480))),
+    "cfg1": dict(
+        desc="Sparse4D default shape as a CSR plan: 6 cams, 4 levels 64x176..8x22, 900 anchors, 13 keypoints, "
+             "C=256, fp32, exact",
+        wl=dict(cameras=6, levels=4, channels=256, queries=900, points_per_query=13, level0_size=(64, 176))),
+    "default": dict(
+        desc="reference BenchWorkload defaults: 6 cams, 4 levels 64x64..8x8, C=256, 900 queries, 13 points",
+        wl=dict()),
+}
+L2_BYTES = 126 * 1024 * 1024
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def measured_peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(config):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get(config)
+        except Exception:
+            return None
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the GPU is busy."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                 "-i", str(self.index), "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, smax, reasons = [], [], set()
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(self.NAMES, parts[2:]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def algorithmic_bytes(gw):
+    """unique touched feature cells x C x 4 + plan inputs + outputs."""
+    wl = gw.workload
+    shape = gw.spatial_shape.reshape(-1, 2)
+    t = gw.camera_ids.astype(np.int64) * wl.levels + gw.levels
+    H = shape[t, 0].astype(np.int64)
+    W = shape[t, 1].astype(np.int64)
+    x0 = np.floor(gw.us).astype(np.int64)
+    y0 = np.floor(gw.vs).astype(np.int64)
+    rows = []
+    for dy in (0, 1):
+        for dx in (0, 1):
+            x, y = x0 + dx, y0 + dy
+            ok = (x >= 0) & (x < W) & (y >= 0) & (y < H)
+            rows.append((gw.tile_start[t] + y * W + x)[ok])
+    touched = np.unique(np.concatenate(rows)).size
+    s_n, q_n = gw.us.size, wl.queries
+    feat_b = touched * wl.channels * 4
+    in_b = s_n * 20 + (q_n + 1) * 8
+    out_b = q_n * wl.channels * 4 + q_n
+    return {"touched_cells": int(touched), "touched_frac": touched / gw.table.shape[0], "feature_bytes": feat_b,
+            "input_bytes": in_b, "output_bytes": out_b, "total": feat_b + in_b + out_b}
+
+
+def cpu_reference_time(gw, budget_s=15.0, reps=3, workers=None):
+    """Time the reference CPU algorithm (oracle port of msda_optimized FULL,
+    all host threads) on a bounded query sample; returns per-full-call seconds."""
+    from oracle import msda_oracle as mo
+
+    workers = workers or os.cpu_count() or 1
+    wl = gw.workload
+    per_q = wl.cameras * wl.levels * wl.points_per_query
+
+    def run(nq):
+        offs = gw.offsets[:nq + 1]
+        s = int(offs[-1])
+        t0 = time.perf_counter()
+        out, _ = mo.msda_tiled(gw.table, gw.tiles, wl.levels, offs, gw.camera_ids[:s], gw.levels[:s], gw.us[:s],
+                               gw.vs[:s], gw.weights[:s], precision="full", workers=workers)
+        return time.perf_counter() - t0, out
+
+    probe = min(wl.queries, max(2 * workers, 32))
+    t_probe, _ = run(probe)  # warm-up + rate probe
+    per_query = t_probe / probe
+    nq = int(min(wl.queries, max(probe, budget_s / reps / max(per_query, 1e-9))))
+    times, out = [], None
+    for _ in range(reps):
+        t, out = run(nq)
+        times.append(t)
+    mean = float(np.mean(times))
+    return {"full_call_s": mean * wl.queries / nq, "sample_queries": nq, "per_q_samples": per_q,
+            "workers": workers, "times_s": times, "out": out}
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    wl = BenchWorkload(**cfg["wl"])
+    gw = generate_workload(wl)
+    workers = os.cpu_count() or 1
+    # size the per-step sample so warmup+steps finish within ~2 minutes
+    r = cpu_reference_time(gw, budget_s=max(1.0, 100.0 / max(1, args.steps + args.warmup)), reps=1,
+                           workers=workers)
+    nq = r["sample_queries"]
+    from oracle import msda_oracle as mo
+
+    s = int(gw.offsets[nq])
+    step = lambda: mo.msda_tiled(gw.table, gw.tiles, wl.levels, gw.offsets[:nq + 1], gw.camera_ids[:s],  # noqa
+                                 gw.levels[:s], gw.us[:s], gw.vs[:s], gw.weights[:s], precision="full",
+                                 workers=workers)
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    t_full = float(np.mean(times)) * wl.queries / nq
+    value = wl.cameras / t_full
+    sample = (f"{nq} of {wl.queries} queries per step ({nq * wl.cameras * wl.levels * wl.points_per_query} "
+              f"samples), extrapolated linearly to the full call")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "camera-frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference generate_workload)",
+        "config": {"workload": args.config, "desc": cfg["desc"], **{k: (list(v) if isinstance(v, tuple) else v)
+                                                                     for k, v in wl.to_dict().items()}},
+        "cpu_baseline": {"value": value, "unit": "camera-frames/s", "cores": workers, "kind": "port",
+                         "sample": sample, "algorithm": "oracle.msda_oracle.msda_tiled (msda_optimized FULL "
+                                                        "restated, numpy, ThreadPool over queries)"},
+        "e2e": {"value": value, "unit": "camera-frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg, rank, local_rank, world):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_10819_b200 import features as F
+    from paper_2601_10819_b200 import ops
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    wl = BenchWorkload(**{**cfg["wl"], "seed": rank})
+    t0 = time.time()
+    host_table = torch.empty((wl.num_rows, wl.channels), dtype=torch.float32, pin_memory=True)
+    gw = generate_workload(wl, table_out=host_table.numpy())
+    log(f"[rank {rank}] workload {args.config}: {wl.num_rows} rows x {wl.channels} ch "
+        f"({host_table.numel() * 4 / 1e9:.2f} GB), {wl.num_samples} samples, generated in {time.time() - t0:.1f}s")
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    feats = ops.DeviceFeatures(host_table.to(dev), t(gw.spatial_shape),
+                               t(gw.tile_start.reshape(wl.cameras, wl.levels)))
+    plan_d = [t(gw.offsets), t(gw.camera_ids), t(gw.levels), t(gw.us), t(gw.vs), t(gw.weights)]
+    out = torch.empty((wl.queries, wl.channels), dtype=torch.float32, device=dev)
+    empty = torch.empty((wl.queries,), dtype=torch.uint8, device=dev)
+    table_bytes = host_table.numel() * 4
+    flush = table_bytes < 2 * L2_BYTES
+    scratch = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev) if flush else None
+
+    # correctness gate (raises on any device status) before timing
+    ops.msda_csr(feats, *plan_d, out=out, empty=empty, check=True)
+
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(max(3, args.warmup)):
+        ops.msda_csr(feats, *plan_d, out=out, empty=empty, check=False)
+    torch.cuda.synchronize(dev)
+
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    smi_index = vis.split(",")[local_rank] if vis else str(local_rank)
+    clocks = ClockSampler(smi_index)
+    clocks.start()
+    time.sleep(0.2)
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    barrier()
+    torch.cuda.synchronize(dev)
+    for k in range(K):
+        if flush:
+            scratch.zero_()
+        ev[k][0].record(stream)
+        ops.msda_csr(feats, *plan_d, out=out, empty=empty, check=False, stages=1)
+        ev[k][1].record(stream)
+        ops.msda_csr(feats, *plan_d, out=out, empty=empty, check=False, stages=2)
+        ev[k][2].record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    # keep the GPU busy a little longer so the clock sampler sees load
+    t_end = time.time() + 0.5
+    while time.time() < t_end:
+        ops.msda_csr(feats, *plan_d, out=out, empty=empty, check=False)
+        torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    plan_ms = [ev[k][0].elapsed_time(ev[k][1]) for k in range(K)]
+    gather_ms = [ev[k][1].elapsed_time(ev[k][2]) for k in range(K)]
+    step_ms = [p + g for p, g in zip(plan_ms, gather_ms)]
+    total_ms = float(np.sum(step_ms))
+    if world > 1:
+        tt = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_per_step = total_ms / K
+    value = world * wl.cameras * K / (total_ms / 1e3)
+
+    # ---- end to end through the reference-facing API (host buffers) ----
+    pyrs = []
+    for c in range(wl.cameras):
+        lv = []
+        for m, (h, w) in enumerate(wl.level_dims()):
+            st = int(gw.tile_start[c * wl.levels + m])
+            lv.append(F.FeatureGrid(stride=wl.strides()[m], values=gw.table[st:st + h * w].reshape(h, w, -1)))
+        pyrs.append(F.FeaturePyramid(c, lv))
+    plan_h = F.SamplePlan.from_csr(gw.offsets, gw.camera_ids, gw.levels, gw.us, gw.vs, gw.weights)
+    e2e_k = max(1, min(K, args.e2e_steps))
+    e2e_times = []
+    for i in range(args.warmup + e2e_k):
+        barrier()
+        t1 = time.perf_counter()
+        out_h, _ = F.msda_optimized(pyrs, plan_h, device=local_rank)
+        dt = time.perf_counter() - t1
+        if i >= args.warmup:
+            e2e_times.append(dt)
+    e2e_s = float(np.mean(e2e_times))
+    if world > 1:
+        tt = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    h2d = table_bytes + gw.us.size * 20 + gw.offsets.size * 8
+    d2h = wl.queries * wl.channels * 4 + wl.queries
+    same = out_h.tobytes() == out.cpu().numpy().tobytes()
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    ab = algorithmic_bytes(gw)
+    peak, peak_src = measured_peak_hbm()
+    g_ms = float(np.mean(gather_ms))
+    achieved = ab["total"] / (g_ms / 1e3) / 1e9
+    call_gbs = ab["total"] / (ms_per_step / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "camera-frames/s", "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference generate_workload bytes, seed=rank)",
+        "config": {"workload": args.config, "desc": cfg["desc"], "precision": "exact (bit-identical)",
+                   "parallelism": f"stream-sharded x{world} (independent scenes, no collective)",
+                   "l2": ("flushed between steps (2x L2 write)" if flush else
+                          f"inputs larger than L2 ({table_bytes / 1e9:.2f} GB table), no flush"),
+                   **{k: (list(v) if isinstance(v, tuple) else v) for k, v in wl.to_dict().items()}},
+        "latency_us": ms_per_step * 1e3,
+        "stage_us": {"plan_canon": float(np.mean(plan_ms)) * 1e3, "gather_exact": g_ms * 1e3},
+        "streams_at_30fps_6layers": int(world * wl.cameras / (30 * 6 * ms_per_step / 1e3)),
+        "call_gbs": call_gbs,
+        "roofline": {"bound": "hbm", "kernel": "gather_exact_kernel<float,4>", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(args.config),
+                     "peak_source": peak_src, "algorithmic_bytes": ab},
+        "e2e": {"value": world * wl.cameras / e2e_s, "unit": "camera-frames/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
+                "api": "paper_2601_10819_b200.features.msda_optimized -> C-ABI msda_csr_host (pinned host buffers)",
+                "bitwise_equal_to_device_path": same},
+        "gpu_launches": 2 * K,
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu:
+        r = cpu_reference_time(gw)
+        nq = r["sample_queries"]
+        parity = r["out"].tobytes() == out.cpu().numpy()[:nq].tobytes()
+        line["cpu_baseline"] = {
+            "value": wl.cameras / r["full_call_s"], "unit": "camera-frames/s", "cores": r["workers"],
+            "kind": "port", "sample": f"{nq} of {wl.queries} queries x3 reps (1 warm-up), extrapolated linearly",
+            "algorithm": "oracle msda_tiled (reference msda_optimized FULL restated, numpy, threads)",
+            "gpu_bitwise_equal_on_sample": bool(parity)}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    rank, local_rank, world = dist_env()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+    else:
+        run_ours(args, cfg, rank, local_rank, world)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,171 @@
+/*
+ * msda_b200 — C ABI of the B200-native Multi-Scale Deformable Aggregation path.
+ *
+ * Drop-in boundary for the reference operator (paths relative to
+ * /root/reference/pkg/src/mvtrack3d/):
+ *
+ *   msda_csr()       replaces msda_reference(pyramids, plan, normalize)      features.py:241-276
+ *                    and      msda_optimized(pyramids, plan, precision,
+ *                                            normalize, workers)           features.py:419-467
+ *   msda_dense()     the Sparse4D operator named by BASELINE north_star:
+ *                    deformable_aggregation(mc_ms_feat, spatial_shape,
+ *                    scale_start_index, sampling_location, weights); the
+ *                    reference has no such symbol, its semantics here are the
+ *                    reference's (zero padding, cell = loc*W - 0.5,
+ *                    features.py:20-24, 184-219) with channel groups G.
+ *   msda_dense_project()  msda_dense with keypoint generation + projection
+ *                    fused in (geometry.py:162-182, 207-255; oae.py:103-111)
+ *   msda_oae_pool()  extract_view_feature + fuse_or_memory (oae.py:81-164)
+ *   msda_csr_host()  msda_csr over HOST buffers (what a ctypes binding of
+ *                    mvtrack3d would call with numpy pointers); copies in and
+ *                    out inside the call.
+ *
+ * Conventions: every pointer is a device pointer unless the entry point says
+ * HOST.  The caller owns every buffer, the workspace and the stream; calls are
+ * asynchronous on `stream` (a cudaStream_t passed as void*), never allocate
+ * (except the context API) and keep no global state.  Argument errors are
+ * returned synchronously; data-dependent errors (zero weight sum, unknown
+ * camera/level, non-finite plan values) are written to a status word in the
+ * workspace and read back with msda_read_status().
+ */
+#ifndef MSDA_B200_H_
+#define MSDA_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; each maps to the reference exception raised for it. */
+enum msda_status {
+  MSDA_OK = 0,
+  MSDA_ODD_CHANNELS = 1,     /* errors.OddChannelCount   features.py:98-99, 441-442        */
+  MSDA_NONFINITE = 2,        /* errors.NonFiniteWeight   features.py:165-166               */
+  MSDA_BAD_TARGET = 3,       /* ValueError unknown camera / missing level  features.py:231-238 */
+  MSDA_ZERO_WEIGHT_SUM = 4,  /* ValueError zero weight sum  features.py:268-269, 285-287   */
+  MSDA_BAD_PRECISION = 5,    /* ValueError unknown precision mode  features.py:443-444     */
+  MSDA_CHANNEL_MISMATCH = 6, /* errors.ChannelMismatch   oae.py:98-100                     */
+  MSDA_CUDA_ERROR = 7,       /* CUDA runtime failure                                       */
+  MSDA_BAD_ARG = 8,          /* shape / pointer / workspace argument error (ValueError)    */
+  MSDA_OFFSET_RANGE = 9      /* errors.OffsetOutOfRange  geometry.py:241-243               */
+};
+
+/* Feature storage dtype. */
+enum msda_dtype { MSDA_F32 = 0, MSDA_F16 = 1, MSDA_BF16 = 2 };
+
+/* Arithmetic mode.
+ *  MSDA_EXACT      f32 arithmetic in the reference's canonical order and
+ *                  expression tree: bit-identical to msda_reference /
+ *                  msda_optimized(FULL) (f32 storage) or to the reference run on
+ *                  features pre-rounded to the storage dtype (f16/bf16).
+ *  MSDA_EXACT_HALF f16 storage and f16 arithmetic/accumulation, bit-identical
+ *                  to msda_optimized(PACKED_HALF) (features.py:306-416).
+ *  MSDA_FAST       FMA arithmetic, any summation order, f32 accumulation;
+ *                  tolerance parity (1e-4 rel. fp32, 1e-2 fp16/bf16).          */
+enum msda_precision { MSDA_EXACT = 0, MSDA_EXACT_HALF = 1, MSDA_FAST = 2 };
+
+/* Multi-camera multi-level feature table: channel-last rows, every
+ * (camera, level) grid (H, W, C) row-major, concatenated camera-major then
+ * level-minor.  `batch` copies of the table are stacked (stride n_rows*C).  */
+typedef struct {
+  const void *data;                 /* [batch, n_rows, channels]                      */
+  int32_t dtype;                    /* enum msda_dtype                               */
+  int32_t batch;                    /* >= 1                                          */
+  int32_t n_cams, n_levels, channels;
+  int32_t reserved;
+  int64_t n_rows;                   /* < 2^31                                        */
+  const int32_t *spatial_shape;     /* [n_cams * n_levels * 2] (H, W)                */
+  const int64_t *scale_start_index; /* [n_cams * n_levels] first row of each grid    */
+} msda_features_t;
+
+/* CSR sample plan (the reference SamplePlan, features.py:112-181).  Camera
+ * ids are given as dense indices 0..n_cams-1 in ascending camera-id order.  */
+typedef struct {
+  int64_t n_queries, n_samples;
+  const int64_t *offsets;      /* [n_queries + 1]                        */
+  const int32_t *camera_index; /* [n_samples]                            */
+  const int32_t *level;        /* [n_samples]                            */
+  const float *u, *v;          /* [n_samples] level-cell coordinates     */
+  const float *weight;         /* [n_samples]                            */
+} msda_csr_plan_t;
+
+/* Pinhole cameras (CameraModel, geometry.py:56-97), float32 on device. */
+typedef struct {
+  const float *K;        /* [n_cams, 4]  fx, fy, cx, cy              */
+  const float *R;        /* [n_cams, 9]  world->camera rotation      */
+  const float *t;        /* [n_cams, 3]  world->camera translation   */
+} msda_cameras_t;
+
+const char *msda_status_string(int32_t status);
+int32_t msda_abi_version(void);
+
+/* Workspace: one device buffer sized by the matching *_workspace_size(). */
+size_t msda_csr_workspace_size(int64_t n_queries, int64_t n_samples, int32_t channels);
+int32_t msda_csr(const msda_features_t *feat, const msda_csr_plan_t *plan, int32_t precision,
+                 int32_t normalize, float *out /* [n_queries, C] */, uint8_t *empty /* [n_queries] */,
+                 void *workspace, size_t workspace_bytes, void *stream);
+
+/* msda_csr split into its two stages (bit 0: canonicalise the plan into the
+ * workspace, bit 1: gather/accumulate from the workspace); msda_csr == mask 3.
+ * Used to time the stages separately.                                       */
+int32_t msda_csr_stages(const msda_features_t *feat, const msda_csr_plan_t *plan, int32_t precision,
+                        int32_t normalize, float *out, uint8_t *empty, void *workspace, size_t workspace_bytes,
+                        void *stream, int32_t stage_mask);
+
+size_t msda_dense_workspace_size(int32_t batch, int32_t n_queries, int32_t n_points, int32_t n_cams,
+                                 int32_t n_levels, int32_t n_groups, int32_t channels);
+/* sampling_location [bs, Q, P, cams, 2] normalized (x, y) in image units,
+ * weights [bs, Q, P, cams, L, G], out [bs, Q, C].  Channel c uses group
+ * c / (C / G).  normalize: divide by the per-(query, group) weight sum.     */
+int32_t msda_dense(const msda_features_t *feat, int32_t n_queries, int32_t n_points, int32_t n_groups,
+                   const float *sampling_location, const float *weights, int32_t precision,
+                   int32_t normalize, float *out, void *workspace, size_t workspace_bytes, void *stream);
+
+/* Fused projection: anchors [bs, Q, 10] (x, y, z, w, l, h, yaw, vx, vy, vz),
+ * learned_offsets [n_learned, 3] in [-1, 1], P = 7 + n_learned keypoints,
+ * motion compensation by velocity*dt, cameras projected in f32, behind-camera
+ * samples (depth <= 1e-6) dropped; image_wh [n_cams, 2] gives the
+ * normalisation; strides [n_levels] the pixel stride per level.
+ * weights [bs, Q, P, cams, L, G].                                           */
+int32_t msda_dense_project(const msda_features_t *feat, int32_t n_queries, const float *anchors,
+                           int32_t n_learned, const float *learned_offsets, const msda_cameras_t *cams,
+                           const float *strides, float dt, int32_t n_groups, const float *weights,
+                           int32_t normalize, float *out, void *workspace, size_t workspace_bytes,
+                           void *stream);
+
+/* OAE pooling (cfg4): per (query, camera) g = softmax_k(desc . g_k / sqrt(D))
+ * weighted keypoint features (level mean), fused over cameras with
+ * visibility weights (invalid views weigh 0), L2-normalised; queries whose
+ * visibility sum is <= 1e-3 get `memory` and all_occluded = 1.
+ * descriptors / memory [Q, D=C], visibility [Q, n_cams], out [Q, C].       */
+int32_t msda_oae_pool(const msda_features_t *feat, int32_t n_queries, const float *anchors,
+                      int32_t n_learned, const float *learned_offsets, const msda_cameras_t *cams,
+                      const float *strides, const float *descriptors, const float *visibility,
+                      const float *memory, float *out, uint8_t *all_occluded, void *workspace,
+                      size_t workspace_bytes, void *stream);
+size_t msda_oae_workspace_size(int32_t n_queries, int32_t n_cams, int32_t channels);
+
+/* Data-dependent status of the last call that used `workspace` (synchronises
+ * `stream`).  detail = offending query / sample index, or -1.               */
+int32_t msda_read_status(const void *workspace, void *stream, int32_t *status, int64_t *detail);
+
+/* ---- host-buffer entry point (end-to-end, copies inside the call) ---- */
+typedef struct msda_context msda_context_t;
+int32_t msda_context_create(int32_t device, msda_context_t **ctx);
+void msda_context_destroy(msda_context_t *ctx);
+/* level_data[t] (HOST) points at grid t = cam*n_levels + level, (H, W, C)
+ * row-major of `dtype`; spatial_shape (HOST) [n_cams*n_levels*2]; the plan
+ * arrays and out / empty are HOST pointers.  Pinned host memory gives
+ * asynchronous full-bandwidth copies; pageable memory works but is staged.  */
+int32_t msda_csr_host(msda_context_t *ctx, const void *const *level_data, const int32_t *spatial_shape,
+                      int32_t n_cams, int32_t n_levels, int32_t channels, int32_t dtype,
+                      int64_t n_queries, const int64_t *offsets, const int32_t *camera_index,
+                      const int32_t *level, const float *u, const float *v, const float *weight,
+                      int32_t precision, int32_t normalize, float *out, uint8_t *empty);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSDA_B200_H_ */

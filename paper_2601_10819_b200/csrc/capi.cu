@@ -1,0 +1,268 @@
+// C ABI of msda_b200 (include/msda_b200.h): argument validation, workspace
+// carving, status mapping and the host-buffer context.  No torch types cross
+// this boundary.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "msda_common.cuh"
+#include "msda_exact.cuh"
+
+using namespace msda;
+
+namespace {
+
+__global__ void f32_to_f16_kernel(const float* __restrict__ src, __half* __restrict__ dst, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __float2half_rn(src[i]);
+}
+
+cudaError_t launch_f32_to_f16(const float* src, __half* dst, int64_t n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 32);
+  f32_to_f16_kernel<<<(unsigned)blocks, 256, 0, s>>>(src, dst, n);
+  return cudaGetLastError();
+}
+
+int g_num_sms_cache[64] = {0};
+
+int num_sms_for_current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (dev >= 0 && dev < 64 && g_num_sms_cache[dev] > 0) return g_num_sms_cache[dev];
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (dev >= 0 && dev < 64) g_num_sms_cache[dev] = n;
+  return n;
+}
+
+int32_t validate_features(const msda_features_t* f) {
+  if (!f || !f->data || !f->spatial_shape || !f->scale_start_index) return MSDA_BAD_ARG;
+  if (f->n_cams <= 0 || f->n_levels <= 0 || f->channels <= 0 || f->batch <= 0) return MSDA_BAD_ARG;
+  if (f->dtype < MSDA_F32 || f->dtype > MSDA_BF16) return MSDA_BAD_ARG;
+  if (f->n_rows <= 0 || f->n_rows >= (int64_t(1) << 31)) return MSDA_BAD_ARG;
+  if (f->channels % 2 != 0) return MSDA_ODD_CHANNELS;
+  return MSDA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t msda_abi_version(void) { return 1; }
+
+const char* msda_status_string(int32_t s) {
+  switch (s) {
+    case MSDA_OK: return "ok";
+    case MSDA_ODD_CHANNELS: return "channel count is odd; packed pairs need an even count";
+    case MSDA_NONFINITE: return "plan weights and coordinates must be finite";
+    case MSDA_BAD_TARGET: return "plan references an unknown camera id or a missing level";
+    case MSDA_ZERO_WEIGHT_SUM: return "plan weights sum to zero, cannot renormalize";
+    case MSDA_BAD_PRECISION: return "unknown precision mode";
+    case MSDA_CHANNEL_MISMATCH: return "pyramid channel count does not match the descriptor length";
+    case MSDA_CUDA_ERROR: return "CUDA runtime error";
+    case MSDA_BAD_ARG: return "invalid argument";
+    case MSDA_OFFSET_RANGE: return "learned keypoint offset component outside [-1, 1]";
+    default: return "unknown status";
+  }
+}
+
+size_t msda_csr_workspace_size(int64_t n_queries, int64_t n_samples, int32_t channels) {
+  (void)channels;
+  return exact_workspace_bytes(n_queries, n_samples);
+}
+
+int32_t msda_csr(const msda_features_t* feat, const msda_csr_plan_t* plan, int32_t precision, int32_t normalize,
+                 float* out, uint8_t* empty, void* workspace, size_t workspace_bytes, void* stream_) {
+  return msda_csr_stages(feat, plan, precision, normalize, out, empty, workspace, workspace_bytes, stream_, 3);
+}
+
+int32_t msda_csr_stages(const msda_features_t* feat, const msda_csr_plan_t* plan, int32_t precision,
+                        int32_t normalize, float* out, uint8_t* empty, void* workspace, size_t workspace_bytes,
+                        void* stream_, int32_t stage_mask) {
+  int32_t st = validate_features(feat);
+  if (st != MSDA_OK) return st;
+  if (!plan || plan->n_queries < 0 || plan->n_samples < 0) return MSDA_BAD_ARG;
+  if (precision != MSDA_EXACT && precision != MSDA_EXACT_HALF && precision != MSDA_FAST) return MSDA_BAD_PRECISION;
+  if (precision == MSDA_EXACT_HALF && feat->dtype != MSDA_F16) return MSDA_BAD_ARG;
+  if (!workspace || workspace_bytes < msda_csr_workspace_size(plan->n_queries, plan->n_samples, feat->channels))
+    return MSDA_BAD_ARG;
+  if (plan->n_queries > 0 && (!plan->offsets || !out)) return MSDA_BAD_ARG;
+  if (plan->n_samples > 0 &&
+      (!plan->camera_index || !plan->level || !plan->u || !plan->v || !plan->weight))
+    return MSDA_BAD_ARG;
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  ExactWorkspace w = carve_exact_workspace(workspace, plan->n_samples);
+  if ((stage_mask & 1) && cudaMemsetAsync(w.status, 0, sizeof(DevStatus), stream) != cudaSuccess)
+    return MSDA_CUDA_ERROR;
+  if (plan->n_queries == 0) return MSDA_OK;
+  // FAST on the CSR path runs the exact kernels: they already sit on the
+  // gather roofline for the reference plan shapes.
+  const int prec = precision == MSDA_FAST ? MSDA_EXACT : precision;
+  if ((stage_mask & 1) &&
+      launch_plan_canon(*feat, *plan, normalize, w, num_sms_for_current_device(), stream) != cudaSuccess)
+    return MSDA_CUDA_ERROR;
+  if ((stage_mask & 2) && launch_gather_exact(*feat, *plan, prec, w, out, empty, stream) != cudaSuccess)
+    return MSDA_CUDA_ERROR;
+  return MSDA_OK;
+}
+
+int32_t msda_read_status(const void* workspace, void* stream_, int32_t* status, int64_t* detail) {
+  if (!workspace) return MSDA_BAD_ARG;
+  DevStatus h{};
+  cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+  if (cudaMemcpyAsync(&h, workspace, sizeof(h), cudaMemcpyDeviceToHost, stream) != cudaSuccess)
+    return MSDA_CUDA_ERROR;
+  if (cudaStreamSynchronize(stream) != cudaSuccess) return MSDA_CUDA_ERROR;
+  if (status) *status = h.code;
+  if (detail) *detail = h.code ? h.detail : -1;
+  return MSDA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// host-buffer context (end-to-end entry point)
+
+struct msda_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+};
+
+int32_t msda_context_create(int32_t device, msda_context_t** ctx) {
+  if (!ctx) return MSDA_BAD_ARG;
+  auto* c = new (std::nothrow) msda_context();
+  if (!c) return MSDA_BAD_ARG;
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return MSDA_CUDA_ERROR;
+  }
+  *ctx = c;
+  return MSDA_OK;
+}
+
+void msda_context_destroy(msda_context_t* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->arena) cudaFree(ctx->arena);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+static int32_t ctx_reserve(msda_context_t* ctx, size_t bytes) {
+  if (bytes <= ctx->arena_bytes) return MSDA_OK;
+  if (ctx->arena) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->arena);
+    ctx->arena = nullptr;
+    ctx->arena_bytes = 0;
+  }
+  size_t want = std::max(bytes, ctx->arena_bytes + ctx->arena_bytes / 2);
+  if (cudaMalloc(&ctx->arena, want) != cudaSuccess) return MSDA_CUDA_ERROR;
+  ctx->arena_bytes = want;
+  return MSDA_OK;
+}
+
+int32_t msda_csr_host(msda_context_t* ctx, const void* const* level_data, const int32_t* spatial_shape,
+                      int32_t n_cams, int32_t n_levels, int32_t channels, int32_t dtype, int64_t n_queries,
+                      const int64_t* offsets, const int32_t* camera_index, const int32_t* level, const float* u,
+                      const float* v, const float* weight, int32_t precision, int32_t normalize, float* out,
+                      uint8_t* empty) {
+  if (!ctx || !level_data || !spatial_shape || !offsets || n_cams <= 0 || n_levels <= 0 || channels <= 0 ||
+      n_queries < 0)
+    return MSDA_BAD_ARG;
+  if (channels % 2) return MSDA_ODD_CHANNELS;
+  if (dtype < MSDA_F32 || dtype > MSDA_BF16) return MSDA_BAD_ARG;
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return MSDA_CUDA_ERROR;
+  const size_t esz = dtype == MSDA_F32 ? 4 : 2;
+  const int n_tiles = n_cams * n_levels;
+  std::vector<int64_t> start(n_tiles);
+  int64_t rows = 0;
+  for (int t = 0; t < n_tiles; ++t) {
+    if (spatial_shape[2 * t] < 0 || spatial_shape[2 * t + 1] < 0) return MSDA_BAD_ARG;
+    if ((int64_t)spatial_shape[2 * t] * spatial_shape[2 * t + 1] > 0 && !level_data[t]) return MSDA_BAD_ARG;
+    start[t] = rows;
+    rows += (int64_t)spatial_shape[2 * t] * spatial_shape[2 * t + 1];
+  }
+  const int64_t S = offsets[n_queries];
+  // PACKED_HALF stores features as f16 (features.py:398): f32 host grids are
+  // copied in and rounded to f16 on the device.
+  const bool cvt_half = (precision == MSDA_EXACT_HALF && dtype == MSDA_F32);
+  const int32_t dev_dtype = cvt_half ? MSDA_F16 : dtype;
+  const size_t half_b = cvt_half ? align_up((size_t)rows * channels * 2, 256) : 0;
+  // arena: [workspace | table | shape | start | offsets | cam | lvl | u | v | w | out | empty]
+  const size_t ws_b = align_up(msda_csr_workspace_size(n_queries, S, channels), 256);
+  const size_t tab_b = align_up((size_t)rows * channels * esz, 256);
+  const size_t shp_b = align_up((size_t)n_tiles * 2 * 4, 256), st_b = align_up((size_t)n_tiles * 8, 256);
+  const size_t off_b = align_up((size_t)(n_queries + 1) * 8, 256), i_b = align_up((size_t)S * 4, 256);
+  const size_t out_b = align_up((size_t)n_queries * channels * 4, 256), emp_b = align_up((size_t)n_queries, 256);
+  const size_t total = ws_b + tab_b + half_b + shp_b + st_b + off_b + 5 * i_b + out_b + emp_b;
+  int32_t st = ctx_reserve(ctx, total);
+  if (st != MSDA_OK) return st;
+  char* p = reinterpret_cast<char*>(ctx->arena);
+  void* d_ws = p; p += ws_b;
+  char* d_tab = p; p += tab_b;
+  char* d_half = p; p += half_b;
+  int32_t* d_shape = reinterpret_cast<int32_t*>(p); p += shp_b;
+  int64_t* d_start = reinterpret_cast<int64_t*>(p); p += st_b;
+  int64_t* d_off = reinterpret_cast<int64_t*>(p); p += off_b;
+  int32_t* d_cam = reinterpret_cast<int32_t*>(p); p += i_b;
+  int32_t* d_lvl = reinterpret_cast<int32_t*>(p); p += i_b;
+  float* d_u = reinterpret_cast<float*>(p); p += i_b;
+  float* d_v = reinterpret_cast<float*>(p); p += i_b;
+  float* d_w = reinterpret_cast<float*>(p); p += i_b;
+  float* d_out = reinterpret_cast<float*>(p); p += out_b;
+  uint8_t* d_emp = reinterpret_cast<uint8_t*>(p);
+  cudaStream_t s = ctx->stream;
+  bool ok = true;
+  for (int t = 0; t < n_tiles && ok; ++t)
+    ok = cudaMemcpyAsync(d_tab + (size_t)start[t] * channels * esz, level_data[t],
+                         (size_t)spatial_shape[2 * t] * spatial_shape[2 * t + 1] * channels * esz,
+                         cudaMemcpyHostToDevice, s) == cudaSuccess;
+  ok = ok && cudaMemcpyAsync(d_shape, spatial_shape, (size_t)n_tiles * 8, cudaMemcpyHostToDevice, s) == cudaSuccess;
+  ok = ok && cudaMemcpyAsync(d_start, start.data(), (size_t)n_tiles * 8, cudaMemcpyHostToDevice, s) == cudaSuccess;
+  ok = ok && cudaMemcpyAsync(d_off, offsets, (size_t)(n_queries + 1) * 8, cudaMemcpyHostToDevice, s) == cudaSuccess;
+  if (S > 0) {
+    ok = ok && cudaMemcpyAsync(d_cam, camera_index, S * 4, cudaMemcpyHostToDevice, s) == cudaSuccess;
+    ok = ok && cudaMemcpyAsync(d_lvl, level, S * 4, cudaMemcpyHostToDevice, s) == cudaSuccess;
+    ok = ok && cudaMemcpyAsync(d_u, u, S * 4, cudaMemcpyHostToDevice, s) == cudaSuccess;
+    ok = ok && cudaMemcpyAsync(d_v, v, S * 4, cudaMemcpyHostToDevice, s) == cudaSuccess;
+    ok = ok && cudaMemcpyAsync(d_w, weight, S * 4, cudaMemcpyHostToDevice, s) == cudaSuccess;
+  }
+  if (!ok) return MSDA_CUDA_ERROR;
+  if (cvt_half) {
+    if (launch_f32_to_f16(reinterpret_cast<const float*>(d_tab), reinterpret_cast<__half*>(d_half),
+                          rows * (int64_t)channels, s) != cudaSuccess)
+      return MSDA_CUDA_ERROR;
+  }
+  msda_features_t f{};
+  f.data = cvt_half ? d_half : d_tab;
+  f.dtype = dev_dtype;
+  f.batch = 1;
+  f.n_cams = n_cams;
+  f.n_levels = n_levels;
+  f.channels = channels;
+  f.n_rows = rows;
+  f.spatial_shape = d_shape;
+  f.scale_start_index = d_start;
+  msda_csr_plan_t pl{n_queries, S, d_off, d_cam, d_lvl, d_u, d_v, d_w};
+  st = msda_csr(&f, &pl, precision, normalize, d_out, d_emp, d_ws, ws_b, s);
+  if (st != MSDA_OK) return st;
+  if (cudaMemcpyAsync(out, d_out, (size_t)n_queries * channels * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return MSDA_CUDA_ERROR;
+  if (empty && cudaMemcpyAsync(empty, d_emp, (size_t)n_queries, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    return MSDA_CUDA_ERROR;
+  int32_t dev_status = 0;
+  int64_t detail = 0;
+  st = msda_read_status(d_ws, s, &dev_status, &detail);
+  if (st != MSDA_OK) return st;
+  return dev_status;
+}
+
+}  // extern "C"

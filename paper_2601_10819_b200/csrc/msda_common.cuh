@@ -1,0 +1,144 @@
+// Shared device helpers for the msda_b200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/msda_b200.h"
+
+namespace msda {
+
+// Per-sample record produced by the plan stage and consumed by the gather
+// stage: absolute feature rows of the four bilinear corners (-1 = outside the
+// grid, reads as zero, features.py:214-217) and the four f32 interpolation
+// weights w00, w10, w01, w11 (features.py:199-208).  32 bytes, 16-B aligned.
+struct __align__(16) SampleRec {
+  int32_t row[4];
+  float iw[4];
+};
+
+// Device status word at the head of every workspace.
+struct DevStatus {
+  int32_t code;
+  int32_t pad;
+  long long detail;
+};
+constexpr size_t kStatusBytes = 256;
+
+__device__ __forceinline__ void set_status(DevStatus* st, int code, long long detail) {
+  if (atomicCAS(&st->code, 0, code) == 0) st->detail = detail;
+}
+
+// Order-preserving float -> uint32 map (ascending float order == ascending
+// key order).  -0.0 is canonicalised to +0.0 first, matching numpy's sort,
+// which treats them as equal (features.py:261-263); all reference arithmetic
+// is insensitive to the sign of a zero coordinate or weight here.
+__device__ __forceinline__ uint32_t ord_f32(float f) {
+  uint32_t b = __float_as_uint(f);
+  if (b == 0x80000000u) b = 0u;
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float unord_f32(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+// Bilinear record for cell coordinates (u, v) on a grid of H x W rows
+// starting at `start`: the float32 arithmetic of features.py:197-208 and the
+// float in-bounds tests of features.py:318-321 (no integer overflow for huge
+// coordinates), separately rounded (no FMA contraction).
+__device__ __forceinline__ SampleRec make_record(float u, float v, int64_t start, int H, int W) {
+  SampleRec r;
+  const float x0f = floorf(u), y0f = floorf(v);
+  const float fu = __fsub_rn(u, x0f), fv = __fsub_rn(v, y0f);
+  const float omu = __fsub_rn(1.0f, fu), omv = __fsub_rn(1.0f, fv);
+  r.iw[0] = __fmul_rn(omu, omv);
+  r.iw[1] = __fmul_rn(fu, omv);
+  r.iw[2] = __fmul_rn(omu, fv);
+  r.iw[3] = __fmul_rn(fu, fv);
+  const bool inx0 = (x0f >= 0.0f) && (x0f <= (float)(W - 1));
+  const bool inx1 = (x0f >= -1.0f) && (x0f <= (float)(W - 2));
+  const bool iny0 = (y0f >= 0.0f) && (y0f <= (float)(H - 1));
+  const bool iny1 = (y0f >= -1.0f) && (y0f <= (float)(H - 2));
+  const int x0 = (inx0 || inx1) ? (int)x0f : 0;
+  const int y0 = (iny0 || iny1) ? (int)y0f : 0;
+  const int64_t base = start + (int64_t)y0 * W + x0;
+  r.row[0] = (inx0 && iny0) ? (int32_t)base : -1;
+  r.row[1] = (inx1 && iny0) ? (int32_t)(base + 1) : -1;
+  r.row[2] = (inx0 && iny1) ? (int32_t)(base + W) : -1;
+  r.row[3] = (inx1 && iny1) ? (int32_t)(base + W + 1) : -1;
+  return r;
+}
+
+// ---- vector loads of VEC channels (read-only, streaming through L1) ----
+template <int BYTES>
+struct RawVec;
+template <>
+struct RawVec<16> { uint4 v; };
+template <>
+struct RawVec<8> { uint2 v; };
+template <>
+struct RawVec<4> { uint32_t v; };
+
+template <int BYTES>
+__device__ __forceinline__ RawVec<BYTES> ldg_vec(const void* p);
+template <>
+__device__ __forceinline__ RawVec<16> ldg_vec<16>(const void* p) {
+  RawVec<16> r;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.v.x), "=r"(r.v.y), "=r"(r.v.z), "=r"(r.v.w)
+               : "l"(p));
+  return r;
+}
+template <>
+__device__ __forceinline__ RawVec<8> ldg_vec<8>(const void* p) {
+  RawVec<8> r;
+  asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.v.x), "=r"(r.v.y) : "l"(p));
+  return r;
+}
+template <>
+__device__ __forceinline__ RawVec<4> ldg_vec<4>(const void* p) {
+  RawVec<4> r;
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(r.v) : "l"(p));
+  return r;
+}
+
+template <int BYTES>
+__device__ __forceinline__ RawVec<BYTES> zero_vec() {
+  RawVec<BYTES> r;
+  uint32_t* w = reinterpret_cast<uint32_t*>(&r);
+#pragma unroll
+  for (int i = 0; i < BYTES / 4; ++i) w[i] = 0u;
+  return r;
+}
+
+// Widen VEC stored elements to f32 (exact for f16 / bf16).
+template <typename T, int VEC>
+__device__ __forceinline__ void to_f32(const RawVec<VEC * sizeof(T)>& r, float* out) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(&r);
+  if constexpr (sizeof(T) == 4) {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) out[i] = __uint_as_float(w[i]);
+  } else if constexpr (std::is_same<T, __half>::value) {
+#pragma unroll
+    for (int i = 0; i < VEC / 2; ++i) {
+      __half2 h = *reinterpret_cast<const __half2*>(&w[i]);
+      float2 f = __half22float2(h);
+      out[2 * i] = f.x;
+      out[2 * i + 1] = f.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < VEC / 2; ++i) {
+      __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+      float2 f = __bfloat1622float2(h);
+      out[2 * i] = f.x;
+      out[2 * i + 1] = f.y;
+    }
+  }
+}
+
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace msda

@@ -1,0 +1,22 @@
+// Internal launch API of the exact CSR path (msda_exact.cu).
+#pragma once
+#include "msda_common.cuh"
+
+namespace msda {
+
+struct ExactWorkspace {
+  DevStatus* status;
+  SampleRec* rec;
+  float* wn;
+  unsigned long long* g_hi;
+  unsigned long long* g_lo;
+};
+
+size_t exact_workspace_bytes(int64_t n_queries, int64_t n_samples);
+ExactWorkspace carve_exact_workspace(void* ws, int64_t n_samples);
+cudaError_t launch_plan_canon(const msda_features_t& f, const msda_csr_plan_t& p, int normalize,
+                              const ExactWorkspace& w, int num_sms, cudaStream_t stream);
+cudaError_t launch_gather_exact(const msda_features_t& f, const msda_csr_plan_t& p, int precision,
+                                const ExactWorkspace& w, float* out, uint8_t* empty, cudaStream_t stream);
+
+}  // namespace msda

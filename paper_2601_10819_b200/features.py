@@ -1,0 +1,278 @@
+"""Drop-in replacement for the reference ``mvtrack3d.features`` hot path.
+
+Same names, argument meaning and error behaviour as
+``/root/reference/pkg/src/mvtrack3d/features.py`` — ``FeatureGrid``,
+``FeaturePyramid``, ``SamplePlan``, ``PrecisionMode``, ``pixel_to_cell``,
+``cell_to_pixel``, ``msda_reference``, ``msda_optimized`` — but the
+aggregation runs on the GPU through the C ABI (``msda_csr_host``: host
+arrays in, host arrays out, copies inside the call).
+
+``msda_optimized(FULL)`` and ``msda_reference`` are bit-identical to the
+reference's (canonical per-query order, same f32 expression tree);
+``msda_optimized(PACKED_HALF)`` is bit-identical to the reference's
+PACKED_HALF.  ``workers`` is accepted and ignored (the output never depends
+on it, features.py:434-436).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+
+from . import _lib as L
+from .errors import NonFiniteWeight, OddChannelCount, raise_for_status
+
+
+class PrecisionMode(Enum):
+    FULL = "full"
+    PACKED_HALF = "half"
+
+
+def pixel_to_cell(pixel: float, stride: float) -> float:
+    """Pixel → level-cell coordinate, cell centres at integers (features.py:45-47)."""
+    return pixel / stride - 0.5
+
+
+def cell_to_pixel(cell: float, stride: float) -> float:
+    return (cell + 0.5) * stride
+
+
+@dataclass(frozen=True)
+class FeatureGrid:
+    """One pyramid level: a read-only (H, W, C) float32 grid (features.py:54-80)."""
+
+    stride: float
+    values: np.ndarray
+
+    def __post_init__(self):
+        vals = np.ascontiguousarray(self.values, dtype=np.float32)
+        if vals.ndim != 3:
+            raise ValueError(f"grid values must be (H, W, C), got shape {vals.shape}")
+        if self.stride <= 0:
+            raise ValueError("stride must be positive")
+        vals.flags.writeable = False
+        object.__setattr__(self, "values", vals)
+
+    @property
+    def height(self) -> int:
+        return self.values.shape[0]
+
+    @property
+    def width(self) -> int:
+        return self.values.shape[1]
+
+    @property
+    def channels(self) -> int:
+        return self.values.shape[2]
+
+
+class FeaturePyramid:
+    """Per-camera levels: shared even C, strictly increasing strides (features.py:83-109)."""
+
+    def __init__(self, camera_id: int, levels):
+        levels = list(levels)
+        if not levels:
+            raise ValueError("a pyramid needs at least one level")
+        channels = levels[0].channels
+        if any(lvl.channels != channels for lvl in levels):
+            raise ValueError("all levels must share one channel count")
+        if channels % 2 != 0:
+            raise OddChannelCount(f"channel count {channels} is odd; packed pairs need an even count")
+        strides = [lvl.stride for lvl in levels]
+        if any(b <= a for a, b in zip(strides, strides[1:])):
+            raise ValueError(f"strides must be strictly increasing, got {strides}")
+        self.camera_id = int(camera_id)
+        self.levels = tuple(levels)
+        self.channels = channels
+
+    def __repr__(self):
+        dims = ", ".join(f"{g.height}x{g.width}" for g in self.levels)
+        return f"FeaturePyramid(camera_id={self.camera_id}, C={self.channels}, levels=[{dims}])"
+
+
+class SamplePlan:
+    """CSR sample tuples (camera_id, level, u, v, weight) (features.py:112-181)."""
+
+    __slots__ = ("offsets", "camera_ids", "levels", "us", "vs", "weights", "num_queries")
+
+    def __init__(self, per_query):
+        counts = [len(s) for s in per_query]
+        offsets = np.zeros(len(counts) + 1, dtype=np.int64)
+        np.cumsum(counts, out=offsets[1:])
+        flat = [t for s in per_query for t in s]
+        cols = list(zip(*flat)) if flat else [(), (), (), (), ()]
+        self._finalize(offsets, np.array(cols[0], dtype=np.int32), np.array(cols[1], dtype=np.int32),
+                       np.array(cols[2], dtype=np.float32), np.array(cols[3], dtype=np.float32),
+                       np.array(cols[4], dtype=np.float32))
+
+    @classmethod
+    def from_arrays(cls, query_index, camera_ids, levels, us, vs, weights, num_queries: int):
+        plan = cls.__new__(cls)
+        qidx = np.asarray(query_index, dtype=np.int64)
+        if qidx.size and (qidx.min() < 0 or qidx.max() >= num_queries):
+            raise ValueError("query_index out of range")
+        counts = np.bincount(qidx, minlength=num_queries)
+        offsets = np.zeros(num_queries + 1, dtype=np.int64)
+        np.cumsum(counts, out=offsets[1:])
+        if qidx.size > 1 and np.any(qidx[1:] < qidx[:-1]):
+            order = np.argsort(qidx, kind="stable")
+            pick = lambda a, dt: np.asarray(a, dtype=dt)[order]  # noqa: E731
+        else:  # already grouped by query: no copy
+            pick = lambda a, dt: np.ascontiguousarray(a, dtype=dt)  # noqa: E731
+        plan._finalize(offsets, pick(camera_ids, np.int32), pick(levels, np.int32), pick(us, np.float32),
+                       pick(vs, np.float32), pick(weights, np.float32))
+        return plan
+
+    @classmethod
+    def from_csr(cls, offsets, camera_ids, levels, us, vs, weights):
+        """Adopt CSR arrays as-is (no copy when dtypes already match)."""
+        plan = cls.__new__(cls)
+        plan._finalize(np.ascontiguousarray(offsets, dtype=np.int64), np.ascontiguousarray(camera_ids, np.int32),
+                       np.ascontiguousarray(levels, np.int32), np.ascontiguousarray(us, np.float32),
+                       np.ascontiguousarray(vs, np.float32), np.ascontiguousarray(weights, np.float32))
+        return plan
+
+    def _finalize(self, offsets, cam, lvl, us, vs, ws):
+        if not (np.isfinite(ws).all() and np.isfinite(us).all() and np.isfinite(vs).all()):
+            raise NonFiniteWeight("plan weights and coordinates must be finite")
+        self.offsets = offsets
+        self.camera_ids = cam
+        self.levels = lvl
+        self.us = us
+        self.vs = vs
+        self.weights = ws
+        self.num_queries = len(offsets) - 1
+
+    @property
+    def num_samples(self) -> int:
+        return int(self.offsets[-1])
+
+    def query_indices(self) -> np.ndarray:
+        return np.repeat(np.arange(self.num_queries, dtype=np.int64), np.diff(self.offsets))
+
+
+# ---------------------------------------------------------------------------
+# host-buffer GPU execution through the C ABI
+
+
+class _Contexts:
+    def __init__(self):
+        self._lock = threading.Lock()
+        self._ctx = {}
+
+    def get(self, device: int):
+        with self._lock:
+            ctx = self._ctx.get(device)
+            if ctx is None:
+                h = ctypes.c_void_p()
+                code = L.lib().msda_context_create(int(device), ctypes.byref(h))
+                raise_for_status(code, -1, "msda_context_create")
+                ctx = h
+                self._ctx[device] = ctx
+            return ctx
+
+
+_CONTEXTS = _Contexts()
+
+
+def _pyramid_map(pyramids) -> dict:
+    out = {}
+    for pyr in pyramids:
+        if pyr.camera_id in out:
+            raise ValueError(f"duplicate camera id {pyr.camera_id}")
+        out[pyr.camera_id] = pyr
+    return out
+
+
+def _ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data) if a.size else ctypes.c_void_p(0)
+
+
+def _prepare(pyr_map, plan: SamplePlan):
+    """Validation of features.py:222-238 + camera-id → dense index mapping."""
+    ids = sorted(pyr_map)
+    chans = {p.channels for p in pyr_map.values()}
+    if len(chans) > 1:
+        raise ValueError("all pyramids must share one channel count")
+    n_levels = max(len(p.levels) for p in pyr_map.values())
+    ragged = any(len(p.levels) != n_levels for p in pyr_map.values())
+    cam = plan.camera_ids
+    if ids == list(range(len(ids))):
+        cam_idx = cam
+        if cam.size and (cam.min() < 0 or cam.max() >= len(ids)):
+            bad = cam[(cam < 0) | (cam >= len(ids))][0]
+            raise ValueError(f"plan references unknown camera id {bad}")
+    else:
+        id_arr = np.asarray(ids, dtype=np.int64)
+        pos = np.searchsorted(id_arr, cam)
+        ok = (pos < len(ids)) & (id_arr[np.minimum(pos, len(ids) - 1)] == cam)
+        if not ok.all():
+            raise ValueError(f"plan references unknown camera id {cam[~ok][0]}")
+        cam_idx = pos.astype(np.int32)
+    lv = plan.levels
+    if lv.size:
+        if ragged:
+            nl = np.array([len(pyr_map[i].levels) for i in ids], dtype=np.int32)
+            if np.any((lv < 0) | (lv >= nl[cam_idx])):
+                raise ValueError("plan references a missing level of a camera")
+        elif lv.min() < 0 or lv.max() >= n_levels:
+            raise ValueError("plan references a missing level of a camera")
+    level_ptrs, shape, keep = [], [], []
+    for i in ids:
+        pyr = pyr_map[i]
+        for m in range(n_levels):
+            if m < len(pyr.levels):
+                g = pyr.levels[m].values
+                keep.append(g)
+                level_ptrs.append(g.ctypes.data)
+                shape += [g.shape[0], g.shape[1]]
+            else:
+                level_ptrs.append(0)
+                shape += [0, 0]
+    return ids, n_levels, chans.pop(), cam_idx, (ctypes.c_void_p * len(level_ptrs))(*level_ptrs), \
+        np.asarray(shape, dtype=np.int32), keep
+
+
+def _run(pyramids, plan: SamplePlan, precision_code: int, normalize: bool, device: int):
+    pyr_map = _pyramid_map(pyramids)
+    q_n = plan.num_queries
+    if not pyr_map:
+        if plan.num_samples:
+            raise ValueError(f"plan references unknown camera id {plan.camera_ids[0]}")
+        return np.zeros((q_n, 0), dtype=np.float32), np.diff(plan.offsets) == 0
+    ids, n_levels, channels, cam_idx, ptrs, shape, keep = _prepare(pyr_map, plan)
+    out = np.empty((q_n, channels), dtype=np.float32)
+    empty = np.empty(q_n, dtype=np.uint8)
+    cam_idx = np.ascontiguousarray(cam_idx, dtype=np.int32)
+    code = L.lib().msda_csr_host(
+        _CONTEXTS.get(device), ptrs, _ptr(shape), len(ids), n_levels, channels, L.MSDA_F32, q_n,
+        _ptr(plan.offsets), _ptr(cam_idx), _ptr(plan.levels), _ptr(plan.us), _ptr(plan.vs), _ptr(plan.weights),
+        precision_code, int(bool(normalize)), _ptr(out), _ptr(empty))
+    del keep
+    raise_for_status(code, -1, "msda")
+    return out, empty.astype(bool)
+
+
+def msda_reference(pyramids, plan: SamplePlan, normalize: bool = True, device: int = 0):
+    """Scalar-semantics MSDA (features.py:241-276), computed on the GPU.
+
+    Bit-identical to the reference's ``msda_reference``.
+    """
+    return _run(pyramids, plan, L.MSDA_EXACT, normalize, device)
+
+
+def msda_optimized(pyramids, plan: SamplePlan, precision: PrecisionMode = PrecisionMode.FULL,
+                   normalize: bool = True, workers: int = 1, device: int = 0):
+    """Batched MSDA (features.py:419-467) on the GPU; same outputs, bit for bit."""
+    pyr_map = _pyramid_map(pyramids)
+    channels = next(iter(pyr_map.values())).channels if pyr_map else 0
+    if channels % 2 != 0:
+        raise OddChannelCount(f"channel count {channels} is odd; packed pairs need an even count")
+    if not isinstance(precision, PrecisionMode):
+        raise ValueError(f"unknown precision mode: {precision!r}")
+    code = L.MSDA_EXACT if precision is PrecisionMode.FULL else L.MSDA_EXACT_HALF
+    return _run(pyramids, plan, code, normalize, device)

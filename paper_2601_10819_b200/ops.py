@@ -1,0 +1,201 @@
+"""Device-tensor API over the C ABI (torch supplies memory and streams only).
+
+All arithmetic happens in ``libmsda_b200.so``; these wrappers validate
+shapes, pass raw device pointers and the current CUDA stream, and map the
+C-ABI status back to the reference's exceptions.
+
+Entry points
+------------
+``DeviceFeatures``          the channel-last multi-camera multi-level table
+``msda_csr``                CSR plan (reference SamplePlan) → out [Q, C], empty [Q]
+``deformable_aggregation``  Sparse4D API (mc_ms_feat, spatial_shape,
+                            scale_start_index, sampling_location, weights)
+``msda_dense_project``      dense path with keypoint projection fused in
+``oae_pool``                occlusion-aware embedding pooling
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib as L
+from .errors import raise_for_status
+
+_DTYPES = {torch.float32: L.MSDA_F32, torch.float16: L.MSDA_F16, torch.bfloat16: L.MSDA_BF16}
+_PREC = {"exact": L.MSDA_EXACT, "exact_half": L.MSDA_EXACT_HALF, "fast": L.MSDA_FAST}
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream(device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+class _Workspace:
+    """Grow-only per-(device, stream) workspace, reused across calls."""
+
+    def __init__(self):
+        self._bufs = {}
+
+    def get(self, device, nbytes):
+        key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+        buf = self._bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+            self._bufs[key] = buf
+        return buf
+
+
+WORKSPACE = _Workspace()
+
+
+def precision_code(precision) -> int:
+    if isinstance(precision, int):
+        return precision
+    try:
+        return _PREC[str(precision)]
+    except KeyError:
+        raise ValueError(f"unknown precision mode: {precision!r}") from None
+
+
+@dataclass
+class DeviceFeatures:
+    """Feature table resident in HBM.
+
+    ``table``: [R, C] or [B, R, C] (f32 / f16 / bf16), rows = every (camera,
+    level) grid (H, W, C) row-major, camera-major then level-minor.
+    ``spatial_shape``: int32 [cams, L, 2] (H, W); ``scale_start_index``:
+    int64 [cams, L] first row of each grid.
+    """
+
+    table: torch.Tensor
+    spatial_shape: torch.Tensor
+    scale_start_index: torch.Tensor
+
+    def __post_init__(self):
+        if self.table.dim() == 2:
+            self.table = self.table.unsqueeze(0)
+        if self.table.dim() != 3 or not self.table.is_cuda or not self.table.is_contiguous():
+            raise ValueError("table must be a contiguous CUDA tensor [R, C] or [B, R, C]")
+        if self.table.dtype not in _DTYPES:
+            raise ValueError(f"unsupported feature dtype {self.table.dtype}")
+        dev = self.table.device
+        self.spatial_shape = self.spatial_shape.to(device=dev, dtype=torch.int32).contiguous()
+        self.scale_start_index = self.scale_start_index.to(device=dev, dtype=torch.int64).contiguous()
+        if self.spatial_shape.dim() != 3 or self.spatial_shape.shape[2] != 2:
+            raise ValueError("spatial_shape must be [cams, levels, 2]")
+        if tuple(self.scale_start_index.shape) != tuple(self.spatial_shape.shape[:2]):
+            raise ValueError("scale_start_index must be [cams, levels]")
+
+    @property
+    def n_cams(self):
+        return int(self.spatial_shape.shape[0])
+
+    @property
+    def n_levels(self):
+        return int(self.spatial_shape.shape[1])
+
+    @property
+    def channels(self):
+        return int(self.table.shape[2])
+
+    def descriptor(self) -> L.Features:
+        return L.Features(_ptr(self.table), _DTYPES[self.table.dtype], int(self.table.shape[0]), self.n_cams,
+                          self.n_levels, self.channels, 0, int(self.table.shape[1]), _ptr(self.spatial_shape),
+                          _ptr(self.scale_start_index))
+
+    @classmethod
+    def from_grids(cls, grids, device="cuda", dtype=torch.float32):
+        """Pack ``[[grid(H, W, C) per level] per camera]`` (numpy or torch)."""
+        rows, shape, start, r = [], [], [], 0
+        for cam in grids:
+            shape.append([])
+            start.append([])
+            for g in cam:
+                g = torch.as_tensor(g)
+                h, w, c = g.shape
+                rows.append(g.reshape(h * w, c))
+                shape[-1].append([h, w])
+                start[-1].append(r)
+                r += h * w
+        table = torch.cat(rows, 0).to(device=device, dtype=dtype).contiguous()
+        return cls(table, torch.tensor(shape, dtype=torch.int32), torch.tensor(start, dtype=torch.int64))
+
+
+def _check_call(code, ws, device, check, what):
+    if code != L.MSDA_OK:
+        raise_for_status(code, -1, what)
+    if check:
+        st, det = ctypes.c_int32(0), ctypes.c_int64(-1)
+        rc = L.lib().msda_read_status(_ptr(ws), _stream(device), ctypes.byref(st), ctypes.byref(det))
+        if rc != L.MSDA_OK:
+            raise_for_status(rc, -1, what)
+        raise_for_status(st.value, det.value, what)
+
+
+def msda_csr(feats: DeviceFeatures, offsets, camera_index, level, u, v, weight, precision="exact",
+             normalize=True, out=None, empty=None, check=True, stages=3):
+    """CSR-plan MSDA on device (``msda_reference`` / ``msda_optimized`` math).
+
+    ``camera_index`` is the dense camera index (ascending camera id).  With
+    ``check`` the call synchronises and raises the reference exception for
+    data-dependent errors; without it the call is fully asynchronous.
+    """
+    dev = feats.table.device
+    q_n = int(offsets.numel()) - 1
+    s_n = int(u.numel())
+    c_n = feats.channels
+    if out is None:
+        out = torch.empty((q_n, c_n), dtype=torch.float32, device=dev)
+    if empty is None:
+        empty = torch.empty((q_n,), dtype=torch.uint8, device=dev)
+    lib = L.lib()
+    nbytes = lib.msda_csr_workspace_size(q_n, s_n, c_n)
+    ws = WORKSPACE.get(dev, nbytes)
+    plan = L.CsrPlan(q_n, s_n, _ptr(offsets), _ptr(camera_index), _ptr(level), _ptr(u), _ptr(v), _ptr(weight))
+    fd = feats.descriptor()
+    code = lib.msda_csr_stages(ctypes.byref(fd), ctypes.byref(plan), precision_code(precision),
+                               int(bool(normalize)), _ptr(out), _ptr(empty), _ptr(ws), ws.numel(), _stream(dev),
+                               int(stages))
+    _check_call(code, ws, dev, check, "msda_csr")
+    return out, empty
+
+
+def deformable_aggregation(mc_ms_feat, spatial_shape, scale_start_index, sampling_location, weights,
+                           precision="fast", normalize=False, out=None, check=False):
+    """Sparse4D ``deformable_aggregation`` (BASELINE north_star API).
+
+    mc_ms_feat [bs, R, C] (f32/f16/bf16), spatial_shape [cams, L, 2],
+    scale_start_index [cams, L], sampling_location [bs, Q, P, cams, 2]
+    (normalized x, y), weights [bs, Q, P, cams, L, G]  →  out [bs, Q, C] f32.
+    Sampling follows the reference convention (cell = loc*W - 0.5, zero
+    padding, features.py:20-24, 184-219).
+    """
+    feats = mc_ms_feat if isinstance(mc_ms_feat, DeviceFeatures) else DeviceFeatures(
+        mc_ms_feat.contiguous(), spatial_shape, scale_start_index)
+    dev = feats.table.device
+    bs, q_n, p_n, cams, two = sampling_location.shape
+    if two != 2 or cams != feats.n_cams:
+        raise ValueError("sampling_location must be [bs, Q, P, cams, 2]")
+    g_n = int(weights.shape[-1])
+    if tuple(weights.shape) != (bs, q_n, p_n, cams, feats.n_levels, g_n):
+        raise ValueError("weights must be [bs, Q, P, cams, levels, groups]")
+    if bs != feats.table.shape[0]:
+        raise ValueError("batch of mc_ms_feat and sampling_location differ")
+    loc = sampling_location.to(torch.float32).contiguous()
+    wts = weights.to(torch.float32).contiguous()
+    if out is None:
+        out = torch.empty((bs, q_n, feats.channels), dtype=torch.float32, device=dev)
+    lib = L.lib()
+    nbytes = lib.msda_dense_workspace_size(bs, q_n, p_n, cams, feats.n_levels, g_n, feats.channels)
+    ws = WORKSPACE.get(dev, nbytes)
+    fd = feats.descriptor()
+    code = lib.msda_dense(ctypes.byref(fd), q_n, p_n, g_n, _ptr(loc), _ptr(wts), precision_code(precision),
+                          int(bool(normalize)), _ptr(out), _ptr(ws), ws.numel(), _stream(dev))
+    _check_call(code, ws, dev, check, "deformable_aggregation")
+    return out

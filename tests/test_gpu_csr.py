@@ -1,0 +1,222 @@
+"""GPU parity of the exact CSR path (C-ABI msda_csr / msda_csr_host).
+
+Oracle: reference outputs (tests/golden, bit for bit) at small sizes; the C
+oracle (oracle/msda_oracle.c, itself pinned to the reference) at the full
+BASELINE sizes.  Bar: bit-identical bytes for FULL and PACKED_HALF.
+"""
+
+import numpy as np
+import pytest
+
+import helpers
+from oracle import msda_oracle as mo
+
+pytestmark = pytest.mark.gpu
+
+
+def _pyramids(F, grids, n_cams, n_levels, ids=None):
+    ids = ids or list(range(n_cams))
+    return [F.FeaturePyramid(ids[c], [F.FeatureGrid(stride=4.0 * 2 ** m, values=grids[(c, m)])
+                                      for m in range(n_levels)]) for c in range(n_cams)]
+
+
+def _gw_pyramids(F, gw):
+    wl = gw.workload
+    pyrs = []
+    for c in range(wl.cameras):
+        lv = []
+        for m, (h, w) in enumerate(wl.level_dims()):
+            st = int(gw.tile_start[c * wl.levels + m])
+            lv.append(F.FeatureGrid(stride=wl.strides()[m], values=gw.table[st:st + h * w].reshape(h, w, -1)))
+        pyrs.append(F.FeaturePyramid(c, lv))
+    return pyrs, F.SamplePlan.from_csr(gw.offsets, gw.camera_ids, gw.levels, gw.us, gw.vs, gw.weights)
+
+
+def test_crit1_workloads_bit_identical(golden, cuda_dev):
+    """Acceptance criterion 1 (test_acceptance.py:94-115) on the GPU: 10^4
+    workloads, FULL bit-identical, PACKED_HALF bit-identical to the reference."""
+    from paper_2601_10819_b200 import features as F
+
+    g = golden("crit1")
+    rng = np.random.default_rng(2024)
+    pos = 0
+    worst = 0.0
+    for i in range(len(g["lens"])):
+        grids, n_cams, n_levels, per_query = helpers.tiny_workload(rng)
+        pyrs = _pyramids(F, grids, n_cams, n_levels)
+        plan = F.SamplePlan(per_query)
+        n = int(g["lens"][i])
+        full, _ = F.msda_optimized(pyrs, plan, F.PrecisionMode.FULL, workers=(1, 2, 4)[i % 3])
+        half, _ = F.msda_optimized(pyrs, plan, F.PrecisionMode.PACKED_HALF)
+        assert full.reshape(-1).tobytes() == g["full"][pos:pos + n].tobytes(), f"workload {i}"
+        assert half.reshape(-1).tobytes() == g["half"][pos:pos + n].tobytes(), f"workload {i} (half)"
+        worst = max(worst, float(np.abs(half.astype(np.float64) - full.astype(np.float64)).max()))
+        pos += n
+    assert worst <= 2e-2
+
+
+def test_features_cases_bit_identical(golden, cuda_dev):
+    from paper_2601_10819_b200 import features as F
+
+    g = golden("features")
+    rng = np.random.default_rng(7)
+    pf = ph = 0
+    for i in range(len(g["lens"])):
+        n_cams, n_levels = int(rng.integers(1, 4)), int(rng.integers(1, 4))
+        channels = int(rng.choice([2, 4, 8, 16]))
+        grids, _ = helpers.make_pyramids(rng, n_cams=n_cams, n_levels=n_levels, channels=channels)
+        per_query = helpers.make_plan(rng, grids, n_queries=int(rng.integers(1, 9)))
+        if i % 7 == 3:
+            per_query.insert(1, [])
+        pyrs = _pyramids(F, grids, n_cams, n_levels)
+        plan = F.SamplePlan(per_query)
+        n = int(g["lens"][i])
+        full, emp = F.msda_reference(pyrs, plan)
+        unn, _ = F.msda_optimized(pyrs, plan, normalize=False)
+        half, _ = F.msda_optimized(pyrs, plan, F.PrecisionMode.PACKED_HALF)
+        assert list(emp) == [len(s) == 0 for s in per_query]
+        assert full.reshape(-1).tobytes() == g["full"][pf:pf + n].tobytes()
+        assert unn.reshape(-1).tobytes() == g["full"][pf + n:pf + 2 * n].tobytes()
+        assert half.reshape(-1).tobytes() == g["half"][ph:ph + n].tobytes()
+        pf += 2 * n
+        ph += n
+
+
+def test_bench_medium_workload(golden, cuda_dev):
+    from paper_2601_10819_b200 import features as F
+    from paper_2601_10819_b200.workload import BenchWorkload, generate_workload
+
+    g = golden("bench")
+    wl = BenchWorkload(cameras=3, levels=4, channels=32, queries=40, points_per_query=13, level0_size=(32, 88))
+    gw = generate_workload(wl)
+    assert gw.checksum == str(g["medium_checksum"])
+    pyrs, plan = _gw_pyramids(F, gw)
+    full, _ = F.msda_optimized(pyrs, plan)
+    half, _ = F.msda_optimized(pyrs, plan, F.PrecisionMode.PACKED_HALF)
+    assert full.tobytes() == g["medium_full"].tobytes()
+    assert half.tobytes() == g["medium_half"].tobytes()
+
+
+@pytest.mark.parametrize("cams,level0", [(6, (64, 176)), (16, (270, 480))])
+def test_full_size_baseline_configs(c_oracle, cuda_dev, cams, level0):
+    """cfg1 / cfg2 at full BASELINE size: GPU bytes == C-oracle bytes."""
+    from paper_2601_10819_b200 import features as F
+    from paper_2601_10819_b200.workload import BenchWorkload, generate_workload
+
+    wl = BenchWorkload(cameras=cams, level0_size=level0)
+    gw = generate_workload(wl)
+    pyrs, plan = _gw_pyramids(F, gw)
+    out, empty = F.msda_optimized(pyrs, plan)
+    ref, ref_empty = c_oracle.msda_c(gw.table, gw.tiles, wl.levels, gw.offsets, gw.camera_ids, gw.levels, gw.us,
+                                     gw.vs, gw.weights)
+    assert out.tobytes() == ref.tobytes()
+    assert not empty.any() and not ref_empty.any()
+    # size-independent property: linearity of the aggregate in the features
+    if cams == 6:
+        half_pyrs = [F.FeaturePyramid(p.camera_id, [F.FeatureGrid(g.stride, g.values * np.float32(0.5))
+                                                    for g in p.levels]) for p in pyrs]
+        out2, _ = F.msda_optimized(half_pyrs, plan)
+        assert out2.tobytes() == (out * np.float32(0.5)).tobytes()  # exact: scaling by 2^-1
+
+
+def test_device_api_and_storage_dtypes(c_oracle, cuda_dev):
+    """ops.msda_csr on device tensors; f16/bf16 storage with f32 math equals
+    the oracle on features pre-rounded to that dtype, bit for bit."""
+    import torch
+
+    from paper_2601_10819_b200 import ops
+    from paper_2601_10819_b200.workload import BenchWorkload, generate_workload
+
+    wl = BenchWorkload(cameras=3, levels=4, channels=64, queries=50, points_per_query=13, level0_size=(40, 96))
+    gw = generate_workload(wl)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(cuda_dev)  # noqa: E731
+    for dt in (torch.float32, torch.float16, torch.bfloat16):
+        table = t(gw.table).to(dt)
+        feats = ops.DeviceFeatures(table, t(gw.spatial_shape), t(gw.tile_start.reshape(wl.cameras, wl.levels)))
+        out, empty = ops.msda_csr(feats, t(gw.offsets), t(gw.camera_ids), t(gw.levels), t(gw.us), t(gw.vs),
+                                  t(gw.weights))
+        rounded = table.float().cpu().numpy()
+        ref, _ = c_oracle.msda_c(rounded, gw.tiles, wl.levels, gw.offsets, gw.camera_ids, gw.levels, gw.us, gw.vs,
+                                 gw.weights)
+        assert out.cpu().numpy().tobytes() == ref.tobytes(), dt
+        if dt is not torch.float32:  # vs unrounded f32 reference: 1e-2 (north_star)
+            full, _ = c_oracle.msda_c(gw.table, gw.tiles, wl.levels, gw.offsets, gw.camera_ids, gw.levels, gw.us,
+                                      gw.vs, gw.weights)
+            assert np.abs(out.cpu().numpy() - full).max() / max(1.0, np.abs(full).max()) <= 1e-2
+
+
+def test_permutation_invariance_bitwise(cuda_dev):
+    from paper_2601_10819_b200 import features as F
+
+    rng = np.random.default_rng(13)
+    grids, _ = helpers.make_pyramids(rng, n_cams=3, n_levels=3, channels=16)
+    per_query = helpers.make_plan(rng, grids, n_queries=20, samples_lo=4, samples_hi=40)
+    pyrs = _pyramids(F, grids, 3, 3)
+    base, _ = F.msda_optimized(pyrs, F.SamplePlan(per_query))
+    for _ in range(5):
+        shuffled = [list(s) for s in per_query]
+        for s in shuffled:
+            rng.shuffle(s)
+        out, _ = F.msda_optimized(pyrs, F.SamplePlan(shuffled))
+        assert out.tobytes() == base.tobytes()
+
+
+def test_long_queries_use_global_sort(c_oracle, cuda_dev):
+    """Queries longer than the shared-memory sort capacity (2048 samples),
+    ties in (cam, level, v, u), duplicate samples, and negative coordinates."""
+    from paper_2601_10819_b200 import features as F
+
+    rng = np.random.default_rng(21)
+    grids, _ = helpers.make_pyramids(rng, n_cams=2, n_levels=2, channels=8, size_lo=5, size_hi=12)
+    per_query = helpers.make_plan(rng, grids, n_queries=3, samples_lo=2500, samples_hi=5000)
+    per_query.append(per_query[0][:10] * 3 + [(0, 0, 1.0, 1.0, 0.5), (0, 0, 1.0, 1.0, 0.25)])
+    pyrs = _pyramids(F, grids, 2, 2)
+    plan = F.SamplePlan(per_query)
+    out, _ = F.msda_optimized(pyrs, plan)
+    table, tiles = mo.pack_grids(grids, 2, 2)
+    ref, _ = c_oracle.msda_c(table, tiles, 2, plan.offsets, plan.camera_ids, plan.levels, plan.us, plan.vs,
+                             plan.weights)
+    assert out.tobytes() == ref.tobytes()
+
+
+def test_camera_ids_need_not_be_dense(cuda_dev):
+    from paper_2601_10819_b200 import features as F
+
+    rng = np.random.default_rng(5)
+    grids, _ = helpers.make_pyramids(rng, n_cams=3, n_levels=2, channels=4)
+    per_query = helpers.make_plan(rng, grids, n_queries=6)
+    ids = [40, 7, 13]  # pyramid order != id order
+    remap = {c: ids[c] for c in range(3)}
+    pq2 = [[(remap[c], m, u, v, w) for c, m, u, v, w in s] for s in per_query]
+    out_dense, _ = F.msda_optimized(_pyramids(F, grids, 3, 2), F.SamplePlan(per_query))
+    # canonical order follows camera *id*, so compare against the oracle with ids ranked
+    rank = {i: r for r, i in enumerate(sorted(ids))}
+    pq_ranked = [[(rank[remap[c]], m, u, v, w) for c, m, u, v, w in s] for s in per_query]
+    grids_ranked = {(rank[remap[c]], m): g for (c, m), g in grids.items()}
+    table, tiles = mo.pack_grids(grids_ranked, 3, 2)
+    ref, _ = mo.msda_exact(table, tiles, 2, *mo.csr_from_per_query(pq_ranked))
+    out, _ = F.msda_optimized(_pyramids(F, grids, 3, 2, ids=ids), F.SamplePlan(pq2))
+    assert out.tobytes() == ref.tobytes()
+    assert out_dense.shape == out.shape
+
+
+def test_errors_match_reference(cuda_dev):
+    from paper_2601_10819_b200 import features as F
+
+    rng = np.random.default_rng(6)
+    grids, _ = helpers.make_pyramids(rng, n_cams=1, n_levels=1)
+    pyrs = _pyramids(F, grids, 1, 1)
+    with pytest.raises(ValueError, match="sum to zero"):
+        F.msda_optimized(pyrs, F.SamplePlan([[(0, 0, 1.0, 1.0, 0.0)]]))
+    with pytest.raises(ValueError):
+        F.msda_optimized(pyrs, F.SamplePlan([[(5, 0, 1.0, 1.0, 1.0)]]))
+    with pytest.raises(ValueError):
+        F.msda_optimized(pyrs, F.SamplePlan([[(0, 3, 1.0, 1.0, 1.0)]]))
+    with pytest.raises(ValueError):
+        F.msda_optimized(pyrs + pyrs, F.SamplePlan([[(0, 0, 1.0, 1.0, 1.0)]]))
+    with pytest.raises(ValueError):
+        F.msda_optimized(pyrs, F.SamplePlan([[(0, 0, 1.0, 1.0, 1.0)]]), precision="full")
+    out, empty = F.msda_optimized(pyrs, F.SamplePlan([[], [(0, 0, 1.0, 1.0, 0.7)], []]))
+    assert list(empty) == [True, False, True]
+    assert not out[0].any() and not out[2].any()
+    np.testing.assert_array_equal(out[1], grids[(0, 0)][1, 1])  # renormalised single weight is exactly 1

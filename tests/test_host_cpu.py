@@ -1,0 +1,96 @@
+"""CPU-only tests: the C-ABI library loads and exports every declared symbol,
+the host-side mirror of the reference API validates like the reference, and
+the product never imports the oracle."""
+
+import ast
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _declared_symbols():
+    hdr = (ROOT / "include" / "msda_b200.h").read_text()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    return sorted(set(re.findall(r"\b(msda_[a-z_]+)\s*\(", hdr)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2601_10819_b200 import _lib
+
+    lib = ctypes.CDLL(str(_lib.LIB_PATH))
+    syms = _declared_symbols()
+    assert len(syms) >= 14
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_lib.SIGNATURES), "ctypes signature table must mirror the header"
+
+
+def test_status_strings_and_abi_version():
+    from paper_2601_10819_b200 import _lib
+
+    assert _lib.lib().msda_abi_version() == 1
+    assert "zero" in _lib.status_string(_lib.MSDA_ZERO_WEIGHT_SUM)
+    assert _lib.status_string(_lib.MSDA_OK) == "ok"
+
+
+def test_argument_errors_without_gpu():
+    """Host-side validation returns before touching the device."""
+    from paper_2601_10819_b200 import _lib
+
+    lib = _lib.lib()
+    f = _lib.Features()
+    p = _lib.CsrPlan()
+    assert lib.msda_csr(ctypes.byref(f), ctypes.byref(p), 0, 1, None, None, None, 0, None) == _lib.MSDA_BAD_ARG
+    f.data = 1
+    f.spatial_shape = 1
+    f.scale_start_index = 1
+    f.n_cams = f.n_levels = f.batch = 1
+    f.channels = 3
+    f.n_rows = 4
+    assert lib.msda_csr(ctypes.byref(f), ctypes.byref(p), 0, 1, None, None, None, 0, None) == _lib.MSDA_ODD_CHANNELS
+    f.channels = 4
+    assert lib.msda_csr(ctypes.byref(f), ctypes.byref(p), 7, 1, None, None, None, 0, None) == _lib.MSDA_BAD_PRECISION
+
+
+def test_reference_mirror_validation():
+    from paper_2601_10819_b200 import features as F
+    from paper_2601_10819_b200.errors import NonFiniteWeight, OddChannelCount
+
+    with pytest.raises(OddChannelCount):
+        F.FeaturePyramid(0, [F.FeatureGrid(stride=8.0, values=np.zeros((2, 2, 3), np.float32))])
+    g = F.FeatureGrid(stride=8.0, values=np.zeros((2, 2, 2), np.float32))
+    with pytest.raises(ValueError):
+        F.FeaturePyramid(0, [g, g])
+    with pytest.raises(ValueError):
+        F.FeatureGrid(stride=0.0, values=np.zeros((2, 2, 2), np.float32))
+    with pytest.raises(NonFiniteWeight):
+        F.SamplePlan([[(0, 0, 1.0, 1.0, np.nan)]])
+    with pytest.raises(NonFiniteWeight):
+        F.SamplePlan([[(0, 0, np.inf, 1.0, 1.0)]])
+    assert F.pixel_to_cell(4.0, 8.0) == 0.0 and F.cell_to_pixel(0.0, 8.0) == 4.0
+    per_query = [[(0, 0, 1.0, 2.0, 0.5), (1, 1, 0.5, 0.5, 0.25)], [], [(0, 1, 3.0, 0.0, 1.0)]]
+    a = F.SamplePlan(per_query)
+    flat = [(q, s) for q, ss in enumerate(per_query) for s in ss]
+    b = F.SamplePlan.from_arrays([q for q, _ in flat][::-1], [s[0] for _, s in flat][::-1],
+                                 [s[1] for _, s in flat][::-1], [s[2] for _, s in flat][::-1],
+                                 [s[3] for _, s in flat][::-1], [s[4] for _, s in flat][::-1], 3)
+    np.testing.assert_array_equal(a.offsets, b.offsets)
+    assert a.num_samples == 3 and list(a.query_indices()) == [0, 0, 2]
+
+
+def test_product_never_imports_oracle():
+    pkg = ROOT / "paper_2601_10819_b200"
+    for py in pkg.rglob("*.py"):
+        tree = ast.parse(py.read_text())
+        for node in ast.walk(tree):
+            names = []
+            if isinstance(node, ast.Import):
+                names = [a.name for a in node.names]
+            elif isinstance(node, ast.ImportFrom):
+                names = [node.module or ""]
+            assert not any(n.split(".")[0] == "oracle" for n in names), f"{py} imports the oracle"
