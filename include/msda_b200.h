@@ -91,11 +91,12 @@ typedef struct {
   const float *weight;         /* [n_samples]                            */
 } msda_csr_plan_t;
 
-/* Pinhole cameras (CameraModel, geometry.py:56-97), float32 on device. */
+/* Pinhole cameras (CameraModel, geometry.py:56-97), float64 on device (the
+ * reference projects in f64; so does the fused kernel). */
 typedef struct {
-  const float *K;        /* [n_cams, 4]  fx, fy, cx, cy              */
-  const float *R;        /* [n_cams, 9]  world->camera rotation      */
-  const float *t;        /* [n_cams, 3]  world->camera translation   */
+  const double *K;       /* [n_cams, 4]  fx, fy, cx, cy              */
+  const double *R;       /* [n_cams, 9]  world->camera rotation      */
+  const double *t;       /* [n_cams, 3]  world->camera translation   */
 } msda_cameras_t;
 
 const char *msda_status_string(int32_t status);
@@ -124,16 +125,17 @@ int32_t msda_dense(const msda_features_t *feat, int32_t n_queries, int32_t n_poi
                    int32_t normalize, float *out, void *workspace, size_t workspace_bytes, void *stream);
 
 /* Fused projection: anchors [bs, Q, 10] (x, y, z, w, l, h, yaw, vx, vy, vz),
- * learned_offsets [n_learned, 3] in [-1, 1], P = 7 + n_learned keypoints,
- * motion compensation by velocity*dt, cameras projected in f32, behind-camera
- * samples (depth <= 1e-6) dropped; image_wh [n_cams, 2] gives the
- * normalisation; strides [n_levels] the pixel stride per level.
- * weights [bs, Q, P, cams, L, G].                                           */
+ * learned_offsets [n_learned, 3] in [-1, 1], P = 7 + n_learned keypoints
+ * (geometry.py:207-247), motion compensation by velocity*dt
+ * (geometry.py:250-255), projection in f64 (geometry.py:162-182) with
+ * behind-camera samples (depth <= 1e-6) dropped from the plan (weight and
+ * contribution); cell = pixel / strides[level] - 0.5 (features.py:45-47).
+ * weights [bs, Q, P, cams, L, G]; workspace = msda_dense_workspace_size(). */
 int32_t msda_dense_project(const msda_features_t *feat, int32_t n_queries, const float *anchors,
                            int32_t n_learned, const float *learned_offsets, const msda_cameras_t *cams,
                            const float *strides, float dt, int32_t n_groups, const float *weights,
-                           int32_t normalize, float *out, void *workspace, size_t workspace_bytes,
-                           void *stream);
+                           int32_t precision, int32_t normalize, float *out, void *workspace,
+                           size_t workspace_bytes, void *stream);
 
 /* OAE pooling (cfg4): per (query, camera) g = softmax_k(desc . g_k / sqrt(D))
  * weighted keypoint features (level mean), fused over cameras with

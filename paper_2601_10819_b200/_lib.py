@@ -58,7 +58,7 @@ SIGNATURES = {
     "msda_dense_workspace_size": (SZ, [I32, I32, I32, I32, I32, I32, I32]),
     "msda_dense": (I32, [ctypes.POINTER(Features), I32, I32, I32, P, P, I32, I32, P, P, SZ, P]),
     "msda_dense_project": (I32, [ctypes.POINTER(Features), I32, P, I32, P, ctypes.POINTER(Cameras), P,
-                                 ctypes.c_float, I32, P, I32, P, P, SZ, P]),
+                                 ctypes.c_float, I32, P, I32, I32, P, P, SZ, P]),
     "msda_oae_pool": (I32, [ctypes.POINTER(Features), I32, P, I32, P, ctypes.POINTER(Cameras), P, P, P, P, P, P,
                             P, SZ, P]),
     "msda_oae_workspace_size": (SZ, [I32, I32, I32]),

@@ -139,6 +139,52 @@ __device__ __forceinline__ void to_f32(const RawVec<VEC * sizeof(T)>& r, float* 
   }
 }
 
+// Keypoint p of an anchor (x, y, z, w, l, h, yaw, vx, vy, vz), float64:
+// p = 0 centre, 1..6 the face centres (+l, -l, +w, -w, +h, -h halves),
+// p >= 7 learned offsets scaled by the half extents (geometry.py:207-247),
+// rotated by yaw, shifted by velocity * dt (geometry.py:250-255).
+// Returns false when a learned offset component leaves [-1, 1].
+__device__ inline bool anchor_keypoint(const float* an, int p, const float* offsets, float dt, double* out) {
+  const double x = an[0], y = an[1], z = an[2], w = an[3], l = an[4], h = an[5], yaw = an[6];
+  const double c = cos(yaw), s = sin(yaw);
+  const double hl = l / 2.0, hw = w / 2.0, hh = h / 2.0;
+  double lx = 0.0, ly = 0.0, lz = 0.0;
+  bool ok = true;
+  switch (p) {
+    case 0: break;
+    case 1: lx = hl; break;
+    case 2: lx = -hl; break;
+    case 3: ly = hw; break;
+    case 4: ly = -hw; break;
+    case 5: lz = hh; break;
+    case 6: lz = -hh; break;
+    default: {
+      const float* o = offsets + (p - 7) * 3;
+      ok = fabsf(o[0]) <= 1.0f && fabsf(o[1]) <= 1.0f && fabsf(o[2]) <= 1.0f;
+      lx = (double)o[0] * hl;
+      ly = (double)o[1] * hw;
+      lz = (double)o[2] * hh;
+    }
+  }
+  out[0] = (c * lx - s * ly) + x + (double)an[7] * (double)dt;
+  out[1] = (s * lx + c * ly) + y + (double)an[8] * (double)dt;
+  out[2] = lz + z + (double)an[9] * (double)dt;
+  return ok;
+}
+
+// Pinhole projection (geometry.py:162-182), float64: p_cam = R p + t; a point
+// with depth <= 1e-6 is behind the camera (returns false); u = fx*x/z + cx.
+__device__ inline bool project_f64(const double* K, const double* R, const double* T, const double* p, double& u,
+                                   double& v) {
+  const double xc = (R[0] * p[0] + R[1] * p[1] + R[2] * p[2]) + T[0];
+  const double yc = (R[3] * p[0] + R[4] * p[1] + R[5] * p[2]) + T[1];
+  const double zc = (R[6] * p[0] + R[7] * p[1] + R[8] * p[2]) + T[2];
+  if (!(zc > 1e-6)) return false;
+  u = K[0] * xc / zc + K[2];
+  v = K[1] * yc / zc + K[3];
+  return true;
+}
+
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 }  // namespace msda

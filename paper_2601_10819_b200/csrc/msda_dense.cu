@@ -1,9 +1,430 @@
-// Placeholder entry points (replaced by the dense / projection / OAE kernels).
+// Dense Sparse4D-layout MSDA (deformable_aggregation) and the fused
+// keypoint-projection variant — sm_100a.
+//
+// FAST mode (the throughput path): one CTA per (batch, anchor).  The CTA
+// walks the anchor's P x cams x L samples in chunks of kChunk:
+//   phase A  all threads build the chunk's 32-B SampleRecs (bilinear corner
+//            rows + f32 interpolation weights; cell = loc*W - 0.5, the
+//            reference convention features.py:20-24) and stage the chunk's
+//            [kChunk, G] group weights in shared memory with coalesced loads.
+//            In PROJECT mode the sample location comes from the anchor's
+//            keypoints (geometry.py:207-255) projected through the camera
+//            (geometry.py:162-182, f64), behind-camera samples get weight 0.
+//   phase B  the CTA is split into n_split sub-groups of C/VEC lanes; each
+//            sub-group takes every n_split-th sample, gathers the four
+//            corner rows with 16-B loads (channel-last rows, full 32-B
+//            sectors) and FMAs them into f32 accumulators with the combined
+//            weights iw_k * w_g.
+// A shared-memory reduction over the sub-groups and the optional
+// per-(anchor, group) renormalisation finish the anchor.
+//
+// EXACT mode expands the dense inputs into one CSR plan per channel group and
+// runs the bit-faithful CSR kernels (msda_exact.cu) on that channel slice.
+#include <algorithm>
+#include <type_traits>
+
 #include "msda_common.cuh"
-extern "C" {
-size_t msda_dense_workspace_size(int32_t, int32_t, int32_t, int32_t, int32_t, int32_t, int32_t) { return 256; }
-int32_t msda_dense(const msda_features_t*, int32_t, int32_t, int32_t, const float*, const float*, int32_t, int32_t, float*, void*, size_t, void*) { return MSDA_BAD_ARG; }
-int32_t msda_dense_project(const msda_features_t*, int32_t, const float*, int32_t, const float*, const msda_cameras_t*, const float*, float, int32_t, const float*, int32_t, float*, void*, size_t, void*) { return MSDA_BAD_ARG; }
-int32_t msda_oae_pool(const msda_features_t*, int32_t, const float*, int32_t, const float*, const msda_cameras_t*, const float*, const float*, const float*, const float*, float*, uint8_t*, void*, size_t, void*) { return MSDA_BAD_ARG; }
-size_t msda_oae_workspace_size(int32_t, int32_t, int32_t) { return 256; }
+#include "msda_exact.cuh"
+
+namespace msda {
+namespace {
+
+constexpr int kDenseThreads = 256;
+constexpr int kChunk = 128;
+constexpr int kMaxGroups = 32;
+constexpr int kMaxPoints = 64;
+
+struct DenseArgs {
+  const void* feat;
+  int64_t n_rows;  // rows per batch item
+  int32_t C, bs, Q, P, cams, L, G;
+  const int32_t* shape;
+  const int64_t* start;
+  const float* loc;  // [bs, Q, P, cams, 2]            (LOC mode)
+  const float* w;    // [bs, Q, P, cams, L, G]
+  int32_t normalize;
+  float* out;        // [bs, Q, C]
+  DevStatus* status;
+  // PROJECT mode
+  const float* anchors;  // [bs, Q, 10]
+  int32_t n_learned;
+  const float* offsets;  // [n_learned, 3]
+  const double* K;       // [cams, 4]
+  const double* R;       // [cams, 9]
+  const double* T;       // [cams, 3]
+  const float* strides;  // [L]
+  float dt;
+};
+
+// Keypoints of one anchor into shared memory (P x 3 doubles).
+__device__ void anchor_keypoints(const DenseArgs& a, int64_t bq, double* kp, DevStatus* st) {
+  for (int p = threadIdx.x; p < a.P; p += blockDim.x)
+    if (!anchor_keypoint(a.anchors + bq * 10, p, a.offsets, a.dt, kp + 3 * p)) set_status(st, MSDA_OFFSET_RANGE, p);
 }
+
+__device__ __forceinline__ bool project_point(const DenseArgs& a, int cam, const double* p, double& u, double& v) {
+  return project_f64(a.K + cam * 4, a.R + cam * 9, a.T + cam * 3, p, u, v);
+}
+
+template <typename T, int VEC, bool PROJECT>
+__global__ void __launch_bounds__(kDenseThreads) dense_fast_kernel(DenseArgs a) {
+  constexpr int BYTES = VEC * (int)sizeof(T);
+  __shared__ SampleRec s_rec[kChunk];
+  __shared__ float s_w[kChunk * kMaxGroups];
+  __shared__ float s_red[kDenseThreads * VEC];
+  __shared__ float s_wsum[kDenseThreads / 2 * 2];
+  __shared__ double s_kp[PROJECT ? kMaxPoints * 3 : 1];
+
+  const int64_t bq = blockIdx.x;  // flattened (batch, anchor)
+  const int b = (int)(bq / a.Q);
+  const int S = a.P * a.cams * a.L;
+  const int lpr = a.C / VEC;                  // lanes per feature row
+  const int n_split = kDenseThreads / lpr;    // sample sub-groups
+  const int sub = threadIdx.x / lpr;
+  const int lane = threadIdx.x - sub * lpr;
+  const bool active = sub < n_split;
+  const int c0 = lane * VEC;
+  const int cpg = a.C / a.G;
+  const int g = c0 / cpg;
+  const bool group_head = (c0 % cpg) == 0;
+  const int64_t row_base = (int64_t)b * a.n_rows;
+  const char* feat = reinterpret_cast<const char*>(a.feat) + (size_t)c0 * sizeof(T);
+  const size_t row_bytes = (size_t)a.C * sizeof(T);
+  const float* wq = a.w + bq * (int64_t)S * a.G;
+
+  if constexpr (PROJECT) {
+    anchor_keypoints(a, bq, s_kp, a.status);
+    __syncthreads();
+  }
+
+  float acc[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) acc[e] = 0.0f;
+  float wsum = 0.0f;
+
+  for (int base = 0; base < S; base += kChunk) {
+    const int n = min(kChunk, S - base);
+    // ---- phase A: records + staged group weights ----
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int s = base + i;
+      const int l = s % a.L;
+      const int pc = s / a.L;
+      const int cam = pc % a.cams;
+      const int p = pc / a.cams;
+      const int t = cam * a.L + l;
+      const int H = a.shape[2 * t], W = a.shape[2 * t + 1];
+      float u, v;
+      bool valid = true;
+      if constexpr (PROJECT) {
+        double up, vp;
+        valid = project_point(a, cam, s_kp + 3 * p, up, vp);
+        const double st = (double)a.strides[l];
+        u = valid ? (float)(up / st - 0.5) : -4.0f;
+        v = valid ? (float)(vp / st - 0.5) : -4.0f;
+      } else {
+        const float* lp = a.loc + ((bq * a.P + p) * a.cams + cam) * 2;
+        u = __fsub_rn(__fmul_rn(lp[0], (float)W), 0.5f);
+        v = __fsub_rn(__fmul_rn(lp[1], (float)H), 0.5f);
+      }
+      SampleRec r = make_record(u, v, row_base + a.start[t], H, W);
+      if (!valid) r.iw[0] = r.iw[1] = r.iw[2] = r.iw[3] = 0.0f;
+      s_rec[i] = r;
+    }
+    for (int j = threadIdx.x; j < n * a.G; j += blockDim.x) s_w[j] = __ldg(wq + (int64_t)base * a.G + j);
+    __syncthreads();
+    if constexpr (PROJECT) {  // behind-camera samples leave the plan: zero weight
+      for (int j = threadIdx.x; j < n * a.G; j += blockDim.x) {
+        const SampleRec& r = s_rec[j / a.G];
+        if (r.iw[0] == 0.0f && r.iw[1] == 0.0f && r.iw[2] == 0.0f && r.iw[3] == 0.0f) s_w[j] = 0.0f;
+      }
+      __syncthreads();
+    }
+    // ---- phase B: gather + FMA ----
+    if (active) {
+      int i = sub;
+      for (; i + n_split < n; i += 2 * n_split) {
+        const SampleRec r0 = s_rec[i], r1 = s_rec[i + n_split];
+        const float w0 = s_w[i * a.G + g], w1 = s_w[(i + n_split) * a.G + g];
+        RawVec<BYTES> c[2][4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          c[0][k] = r0.row[k] >= 0 ? ldg_vec<BYTES>(feat + (size_t)r0.row[k] * row_bytes) : zero_vec<BYTES>();
+          c[1][k] = r1.row[k] >= 0 ? ldg_vec<BYTES>(feat + (size_t)r1.row[k] * row_bytes) : zero_vec<BYTES>();
+        }
+        wsum += w0 + w1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float f0[VEC], f1[VEC];
+          to_f32<T, VEC>(c[0][k], f0);
+          to_f32<T, VEC>(c[1][k], f1);
+          const float cw0 = r0.iw[k] * w0, cw1 = r1.iw[k] * w1;
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc[e] = fmaf(f1[e], cw1, fmaf(f0[e], cw0, acc[e]));
+        }
+      }
+      for (; i < n; i += n_split) {
+        const SampleRec r0 = s_rec[i];
+        const float w0 = s_w[i * a.G + g];
+        wsum += w0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (r0.row[k] < 0) continue;
+          float f0[VEC];
+          to_f32<T, VEC>(ldg_vec<BYTES>(feat + (size_t)r0.row[k] * row_bytes), f0);
+          const float cw0 = r0.iw[k] * w0;
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc[e] = fmaf(f0[e], cw0, acc[e]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- reduce sub-groups, renormalise, write ----
+  if (active) {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) s_red[sub * a.C + c0 + e] = acc[e];
+    if (group_head) s_wsum[sub * a.G + g] = wsum;
+  }
+  __syncthreads();
+  float* o = a.out + bq * a.C;
+  for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
+    float sum = 0.0f;
+    for (int j = 0; j < n_split; ++j) sum += s_red[j * a.C + c];
+    if (a.normalize) {
+      const int gg = c / cpg;
+      float ws = 0.0f;
+      for (int j = 0; j < n_split; ++j) ws += s_wsum[j * a.G + gg];
+      if (ws == 0.0f) set_status(a.status, MSDA_ZERO_WEIGHT_SUM, bq);
+      sum = sum / ws;
+    }
+    o[c] = sum;
+  }
+}
+
+template <typename T, int VEC, bool PROJECT>
+cudaError_t launch_dense_fast_t(const DenseArgs& a, cudaStream_t s) {
+  const int64_t grid = (int64_t)a.bs * a.Q;
+  if (grid == 0) return cudaSuccess;
+  dense_fast_kernel<T, VEC, PROJECT><<<(unsigned)grid, kDenseThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <bool PROJECT>
+cudaError_t launch_dense_fast(const DenseArgs& a, int dtype, cudaStream_t s) {
+  const int cpg = a.C / a.G;
+  const auto fits = [&](int vec) { return a.C % vec == 0 && cpg % vec == 0 && a.C / vec <= kDenseThreads; };
+  switch (dtype) {
+    case MSDA_F32:
+      if (fits(4)) return launch_dense_fast_t<float, 4, PROJECT>(a, s);
+      return launch_dense_fast_t<float, 2, PROJECT>(a, s);
+    case MSDA_F16:
+      if (fits(8)) return launch_dense_fast_t<__half, 8, PROJECT>(a, s);
+      if (fits(4)) return launch_dense_fast_t<__half, 4, PROJECT>(a, s);
+      return launch_dense_fast_t<__half, 2, PROJECT>(a, s);
+    default:
+      if (fits(8)) return launch_dense_fast_t<__nv_bfloat16, 8, PROJECT>(a, s);
+      if (fits(4)) return launch_dense_fast_t<__nv_bfloat16, 4, PROJECT>(a, s);
+      return launch_dense_fast_t<__nv_bfloat16, 2, PROJECT>(a, s);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// EXACT: dense -> CSR plan for one channel group
+
+template <bool PROJECT>
+__global__ void dense_expand_kernel(DenseArgs a, int group, int64_t* offsets, int32_t* cam_o, int32_t* lvl_o,
+                                    float* u_o, float* v_o, float* w_o) {
+  __shared__ double s_kp[PROJECT ? kMaxPoints * 3 : 1];
+  const int S = a.P * a.cams * a.L;
+  const int64_t bq = blockIdx.x;
+  if constexpr (PROJECT) {
+    anchor_keypoints(a, bq, s_kp, a.status);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    offsets[bq] = bq * S;
+    if (bq == (int64_t)a.bs * a.Q - 1) offsets[bq + 1] = (bq + 1) * S;
+  }
+  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+    const int l = s % a.L;
+    const int pc = s / a.L;
+    const int cam = pc % a.cams;
+    const int p = pc / a.cams;
+    const int t = cam * a.L + l;
+    const int64_t o = bq * S + s;
+    float u, v, w = a.w[o * a.G + group];
+    if constexpr (PROJECT) {
+      double up, vp;
+      if (project_point(a, cam, s_kp + 3 * p, up, vp)) {
+        const double st = (double)a.strides[l];
+        u = (float)(up / st - 0.5);
+        v = (float)(vp / st - 0.5);
+      } else {  // behind the camera: a zero-weight, fully outside sample adds nothing
+        u = v = -4.0f;
+        w = 0.0f;
+      }
+    } else {
+      const float* lp = a.loc + ((bq * a.P + p) * a.cams + cam) * 2;
+      u = __fsub_rn(__fmul_rn(lp[0], (float)a.shape[2 * t + 1]), 0.5f);
+      v = __fsub_rn(__fmul_rn(lp[1], (float)a.shape[2 * t]), 0.5f);
+    }
+    cam_o[o] = cam;
+    lvl_o[o] = l;
+    u_o[o] = u;
+    v_o[o] = v;
+    w_o[o] = w;
+  }
+}
+
+size_t dense_exact_extra_bytes(int64_t n_queries, int64_t n_samples) {
+  return align_up((size_t)(n_queries + 1) * 8, 256) + 5 * align_up((size_t)n_samples * 4, 256);
+}
+
+int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, const float* loc, const float* w,
+                  int32_t precision, int32_t normalize, float* out, void* ws, size_t ws_bytes, cudaStream_t s,
+                  bool project, const float* anchors, int32_t n_learned, const float* offsets,
+                  const msda_cameras_t* cams, const float* strides, float dt);
+
+}  // namespace
+}  // namespace msda
+
+using namespace msda;
+
+namespace {
+
+int32_t validate_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G) {
+  if (!f || !f->data || !f->spatial_shape || !f->scale_start_index) return MSDA_BAD_ARG;
+  if (f->n_cams <= 0 || f->n_levels <= 0 || f->channels <= 0 || f->batch <= 0 || Q < 0 || P <= 0) return MSDA_BAD_ARG;
+  if (f->dtype < MSDA_F32 || f->dtype > MSDA_BF16) return MSDA_BAD_ARG;
+  if (f->channels % 2) return MSDA_ODD_CHANNELS;
+  if (G <= 0 || G > kMaxGroups || f->channels % G || (f->channels / G) % 2) return MSDA_BAD_ARG;
+  if (f->n_rows <= 0 || (int64_t)f->batch * f->n_rows >= (int64_t(1) << 31)) return MSDA_BAD_ARG;
+  const int esz = f->dtype == MSDA_F32 ? 4 : 2;
+  if (f->channels / 2 > kDenseThreads || (reinterpret_cast<uintptr_t>(f->data) % 4) || (f->channels * esz) % 4)
+    return MSDA_BAD_ARG;
+  return MSDA_OK;
+}
+
+size_t dense_ws(int32_t batch, int32_t Q, int32_t P, int32_t cams, int32_t L) {
+  const int64_t nq = (int64_t)batch * Q;
+  const int64_t S = nq * P * cams * L;
+  return exact_workspace_bytes(nq, S) + dense_exact_extra_bytes(nq, S);
+}
+
+}  // namespace
+
+namespace msda {
+namespace {
+
+int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, const float* loc, const float* w,
+                  int32_t precision, int32_t normalize, float* out, void* ws, size_t ws_bytes, cudaStream_t s,
+                  bool project, const float* anchors, int32_t n_learned, const float* offsets,
+                  const msda_cameras_t* cams, const float* strides, float dt) {
+  DenseArgs a{};
+  a.feat = f->data;
+  a.n_rows = f->n_rows;
+  a.C = f->channels;
+  a.bs = f->batch;
+  a.Q = Q;
+  a.P = P;
+  a.cams = f->n_cams;
+  a.L = f->n_levels;
+  a.G = G;
+  a.shape = f->spatial_shape;
+  a.start = f->scale_start_index;
+  a.loc = loc;
+  a.w = w;
+  a.normalize = normalize;
+  a.out = out;
+  if (project) {
+    a.anchors = anchors;
+    a.n_learned = n_learned;
+    a.offsets = offsets;
+    a.K = reinterpret_cast<const double*>(cams->K);
+    a.R = reinterpret_cast<const double*>(cams->R);
+    a.T = reinterpret_cast<const double*>(cams->t);
+    a.strides = strides;
+    a.dt = dt;
+  }
+  const int64_t nq = (int64_t)a.bs * Q;
+  const int64_t S = nq * P * a.cams * a.L;
+  if (ws_bytes < exact_workspace_bytes(nq, S) + dense_exact_extra_bytes(nq, S)) return MSDA_BAD_ARG;
+  ExactWorkspace ew = carve_exact_workspace(ws, S);
+  a.status = ew.status;
+  if (cudaMemsetAsync(ew.status, 0, sizeof(DevStatus), s) != cudaSuccess) return MSDA_CUDA_ERROR;
+  if (nq == 0) return MSDA_OK;
+  if (precision == MSDA_FAST) {
+    const cudaError_t e = project ? launch_dense_fast<true>(a, f->dtype, s) : launch_dense_fast<false>(a, f->dtype, s);
+    return e == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
+  }
+  if (precision == MSDA_EXACT_HALF && f->dtype != MSDA_F16) return MSDA_BAD_ARG;
+  // EXACT / EXACT_HALF: one canonical CSR plan per group, exact kernels on its channel slice
+  char* p = reinterpret_cast<char*>(ws) + exact_workspace_bytes(nq, S);
+  int64_t* d_off = reinterpret_cast<int64_t*>(p);
+  p += align_up((size_t)(nq + 1) * 8, 256);
+  const size_t sb = align_up((size_t)S * 4, 256);
+  int32_t* d_cam = reinterpret_cast<int32_t*>(p);
+  int32_t* d_lvl = reinterpret_cast<int32_t*>(p + sb);
+  float* d_u = reinterpret_cast<float*>(p + 2 * sb);
+  float* d_v = reinterpret_cast<float*>(p + 3 * sb);
+  float* d_w = reinterpret_cast<float*>(p + 4 * sb);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  msda_csr_plan_t plan{nq, S, d_off, d_cam, d_lvl, d_u, d_v, d_w};
+  const int cpg = a.C / G;
+  for (int g = 0; g < G; ++g) {
+    if (project)
+      dense_expand_kernel<true><<<(unsigned)nq, 256, 0, s>>>(a, g, d_off, d_cam, d_lvl, d_u, d_v, d_w);
+    else
+      dense_expand_kernel<false><<<(unsigned)nq, 256, 0, s>>>(a, g, d_off, d_cam, d_lvl, d_u, d_v, d_w);
+    if (cudaGetLastError() != cudaSuccess) return MSDA_CUDA_ERROR;
+    if (launch_plan_canon(*f, plan, normalize, ew, sms, s, Q) != cudaSuccess) return MSDA_CUDA_ERROR;
+    if (launch_gather_exact(*f, plan, precision, ew, out, nullptr, s, g * cpg, cpg) != cudaSuccess)
+      return MSDA_CUDA_ERROR;
+  }
+  return MSDA_OK;
+}
+
+}  // namespace
+}  // namespace msda
+
+extern "C" {
+
+size_t msda_dense_workspace_size(int32_t batch, int32_t n_queries, int32_t n_points, int32_t n_cams,
+                                 int32_t n_levels, int32_t n_groups, int32_t channels) {
+  (void)n_groups;
+  (void)channels;
+  return dense_ws(batch, n_queries, n_points, n_cams, n_levels);
+}
+
+int32_t msda_dense(const msda_features_t* feat, int32_t n_queries, int32_t n_points, int32_t n_groups,
+                   const float* sampling_location, const float* weights, int32_t precision, int32_t normalize,
+                   float* out, void* workspace, size_t workspace_bytes, void* stream) {
+  int32_t st = validate_dense(feat, n_queries, n_points, n_groups);
+  if (st != MSDA_OK) return st;
+  if (precision < MSDA_EXACT || precision > MSDA_FAST) return MSDA_BAD_PRECISION;
+  if (!sampling_location || !weights || !out || !workspace) return MSDA_BAD_ARG;
+  return run_dense(feat, n_queries, n_points, n_groups, sampling_location, weights, precision, normalize, out,
+                   workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream), false, nullptr, 0, nullptr,
+                   nullptr, nullptr, 0.0f);
+}
+
+int32_t msda_dense_project(const msda_features_t* feat, int32_t n_queries, const float* anchors, int32_t n_learned,
+                           const float* learned_offsets, const msda_cameras_t* cams, const float* strides, float dt,
+                           int32_t n_groups, const float* weights, int32_t precision, int32_t normalize, float* out,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  const int32_t P = 7 + n_learned;
+  int32_t st = validate_dense(feat, n_queries, P, n_groups);
+  if (st != MSDA_OK) return st;
+  if (precision < MSDA_EXACT || precision > MSDA_FAST) return MSDA_BAD_PRECISION;
+  if (n_learned < 0 || P > kMaxPoints || (n_learned > 0 && !learned_offsets)) return MSDA_BAD_ARG;
+  if (!anchors || !cams || !cams->K || !cams->R || !cams->t || !strides || !weights || !out || !workspace)
+    return MSDA_BAD_ARG;
+  return run_dense(feat, n_queries, P, n_groups, nullptr, weights, precision, normalize, out, workspace,
+                   workspace_bytes, reinterpret_cast<cudaStream_t>(stream), true, anchors, n_learned,
+                   learned_offsets, cams, strides, dt);
+}
+
+}  // extern "C"

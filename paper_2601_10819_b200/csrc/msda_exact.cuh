@@ -15,8 +15,10 @@ struct ExactWorkspace {
 size_t exact_workspace_bytes(int64_t n_queries, int64_t n_samples);
 ExactWorkspace carve_exact_workspace(void* ws, int64_t n_samples);
 cudaError_t launch_plan_canon(const msda_features_t& f, const msda_csr_plan_t& p, int normalize,
-                              const ExactWorkspace& w, int num_sms, cudaStream_t stream);
+                              const ExactWorkspace& w, int num_sms, cudaStream_t stream,
+                              int64_t queries_per_batch = 0);
 cudaError_t launch_gather_exact(const msda_features_t& f, const msda_csr_plan_t& p, int precision,
-                                const ExactWorkspace& w, float* out, uint8_t* empty, cudaStream_t stream);
+                                const ExactWorkspace& w, float* out, uint8_t* empty, cudaStream_t stream,
+                                int c_off = 0, int c_count = 0);
 
 }  // namespace msda

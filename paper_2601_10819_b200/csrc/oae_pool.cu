@@ -1,0 +1,252 @@
+// Occlusion-aware embedding pooling (cfg4), fused after the keypoint
+// sampling — sm_100a.
+//
+// Restates mvtrack3d.oae (oae.py:81-164) on the device, one CTA per query:
+//   for every camera
+//     for every keypoint (geometry.py:207-255 in f64) in front of the camera
+//       g_k = mean over levels of the f32 bilinear read at
+//             cell = pixel / stride - 0.5                  (oae.py:103-112)
+//     a = softmax_k(desc . g_k / sqrt(D)); view = sum_k a_k g_k (oae.py:117-122)
+//   fused = sum_c v_c view_c / sum_c v_c over valid views    (oae.py:125-151)
+//   |fused|_2 normalised; sum v <= 1e-3 -> memory, all_occluded (oae.py:154-164)
+// Threads own VEC consecutive channels (16-B gathers of channel-last rows);
+// g_k lives in shared memory in f64, dot products are block reductions.
+#include <algorithm>
+
+#include "msda_common.cuh"
+
+namespace msda {
+namespace {
+
+constexpr int kOaeMaxPoints = 64;
+constexpr int kOaeMaxC = 1024;
+
+struct OaeArgs {
+  const void* feat;
+  int32_t C, cams, L, Q;
+  const int32_t* shape;
+  const int64_t* start;
+  const float* anchors;  // [Q, 10]
+  const float* offsets;  // [n_learned, 3]
+  int32_t P;
+  const double* K;
+  const double* R;
+  const double* T;
+  const float* strides;  // [L]
+  const float* desc;     // [Q, C]
+  const float* vis;      // [Q, cams]
+  const float* memory;   // [Q, C]
+  float* out;            // [Q, C]
+  uint8_t* occluded;     // [Q]
+  DevStatus* status;
+};
+
+// block-wide sum of one double per thread (blockDim multiple of 32, <= 1024)
+__device__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+  return s;
+}
+
+template <typename T, int VEC>
+__global__ void oae_pool_kernel(OaeArgs a) {
+  constexpr int BYTES = VEC * (int)sizeof(T);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* s_g = reinterpret_cast<double*>(smem_raw);  // [P][C]
+  __shared__ double s_kp[kOaeMaxPoints * 3];
+  __shared__ double s_red[32];
+  __shared__ double s_score[kOaeMaxPoints];
+  __shared__ int s_valid[kOaeMaxPoints];
+
+  const int q = blockIdx.x;
+  const int c0 = threadIdx.x * VEC;
+  const bool active = c0 < a.C;
+  const size_t row_bytes = (size_t)a.C * sizeof(T);
+  const char* feat = reinterpret_cast<const char*>(a.feat) + (size_t)(active ? c0 : 0) * sizeof(T);
+
+  for (int p = threadIdx.x; p < a.P; p += blockDim.x)
+    if (!anchor_keypoint(a.anchors + (int64_t)q * 10, p, a.offsets, 0.0f, s_kp + 3 * p))
+      set_status(a.status, MSDA_OFFSET_RANGE, p);
+  __syncthreads();
+
+  double d[VEC], fused[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    d[e] = active ? (double)a.desc[(int64_t)q * a.C + c0 + e] : 0.0;
+    fused[e] = 0.0;
+  }
+  const double inv_sqrt_d = 1.0 / sqrt((double)a.C);
+  double vis_total = 0.0;
+
+  for (int cam = 0; cam < a.cams; ++cam) {
+    int n_valid = 0;
+    for (int p = 0; p < a.P; ++p) {
+      double up, vp;
+      const bool ok = project_f64(a.K + cam * 4, a.R + cam * 9, a.T + cam * 3, s_kp + 3 * p, up, vp);
+      if (threadIdx.x == 0) s_valid[p] = ok;
+      if (!ok) continue;
+      ++n_valid;
+      double g[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) g[e] = 0.0;
+      for (int l = 0; l < a.L; ++l) {
+        const int t = cam * a.L + l;
+        const double st = (double)a.strides[l];
+        const SampleRec r = make_record((float)(up / st - 0.5), (float)(vp / st - 0.5), a.start[t],
+                                        a.shape[2 * t], a.shape[2 * t + 1]);
+        float c[4][VEC];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const RawVec<BYTES> raw = (active && r.row[k] >= 0) ? ldg_vec<BYTES>(feat + (size_t)r.row[k] * row_bytes)
+                                                              : zero_vec<BYTES>();
+          to_f32<T, VEC>(raw, c[k]);
+        }
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          const float b = __fadd_rn(__fadd_rn(__fmul_rn(c[0][e], r.iw[0]), __fmul_rn(c[1][e], r.iw[1])),
+                                    __fadd_rn(__fmul_rn(c[2][e], r.iw[2]), __fmul_rn(c[3][e], r.iw[3])));
+          g[e] += (double)b;
+        }
+      }
+      double dot = 0.0;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        g[e] /= (double)a.L;  // level mean (oae.py:112)
+        if (active) s_g[(size_t)p * a.C + c0 + e] = g[e];
+        dot += g[e] * d[e];
+      }
+      dot = block_sum(dot, s_red);
+      if (threadIdx.x == 0) s_score[p] = dot * inv_sqrt_d;
+    }
+    __syncthreads();
+    if (n_valid == 0) continue;  // invalid view: zero visibility weight (oae.py:141-143)
+    double mx = -INFINITY;
+    for (int p = 0; p < a.P; ++p)
+      if (s_valid[p]) mx = fmax(mx, s_score[p]);
+    double z = 0.0;
+    for (int p = 0; p < a.P; ++p)
+      if (s_valid[p]) z += exp(s_score[p] - mx);
+    double view[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) view[e] = 0.0;
+    for (int p = 0; p < a.P; ++p) {
+      if (!s_valid[p]) continue;
+      const double wgt = exp(s_score[p] - mx) / z;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e)
+        if (active) view[e] += wgt * s_g[(size_t)p * a.C + c0 + e];
+    }
+    const double v = (double)a.vis[(int64_t)q * a.cams + cam];
+    vis_total += v;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) fused[e] += v * view[e];
+    __syncthreads();
+  }
+
+  float* o = a.out + (int64_t)q * a.C;
+  if (!(vis_total > 1e-3)) {  // AllOccluded -> keep the memory embedding
+    if (active)
+      for (int e = 0; e < VEC; ++e) o[c0 + e] = a.memory[(int64_t)q * a.C + c0 + e];
+    if (threadIdx.x == 0) a.occluded[q] = 1;
+    return;
+  }
+  double sq = 0.0;
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    fused[e] /= vis_total;
+    sq += fused[e] * fused[e];
+  }
+  const double norm = sqrt(block_sum(active ? sq : 0.0, s_red));
+  if (!(norm >= 1e-12)) set_status(a.status, MSDA_BAD_ARG, q);  // cannot normalise (oae.py:47-49)
+  if (active)
+    for (int e = 0; e < VEC; ++e) o[c0 + e] = (float)(fused[e] / norm);
+  if (threadIdx.x == 0) a.occluded[q] = 0;
+}
+
+template <typename T, int VEC>
+cudaError_t launch_oae_t(const OaeArgs& a, cudaStream_t s) {
+  const int lanes = a.C / VEC;
+  const int block = std::max(32, (lanes + 31) / 32 * 32);
+  const size_t smem = (size_t)a.P * a.C * sizeof(double);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(oae_pool_kernel<T, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  if (a.Q == 0) return cudaSuccess;
+  oae_pool_kernel<T, VEC><<<a.Q, block, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+}  // namespace msda
+
+using namespace msda;
+
+extern "C" {
+
+size_t msda_oae_workspace_size(int32_t n_queries, int32_t n_cams, int32_t channels) {
+  (void)n_queries;
+  (void)n_cams;
+  (void)channels;
+  return kStatusBytes;
+}
+
+int32_t msda_oae_pool(const msda_features_t* f, int32_t n_queries, const float* anchors, int32_t n_learned,
+                      const float* learned_offsets, const msda_cameras_t* cams, const float* strides,
+                      const float* descriptors, const float* visibility, const float* memory, float* out,
+                      uint8_t* all_occluded, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!f || !f->data || !f->spatial_shape || !f->scale_start_index || f->batch != 1) return MSDA_BAD_ARG;
+  if (f->n_cams <= 0 || f->n_levels <= 0 || f->channels <= 0 || n_queries < 0 || n_learned < 0) return MSDA_BAD_ARG;
+  if (f->channels % 2) return MSDA_ODD_CHANNELS;
+  if (f->channels > kOaeMaxC || 7 + n_learned > kOaeMaxPoints) return MSDA_BAD_ARG;
+  if (!anchors || !cams || !cams->K || !cams->R || !cams->t || !strides || !descriptors || !visibility ||
+      !memory || !out || !all_occluded || !workspace || workspace_bytes < kStatusBytes)
+    return MSDA_BAD_ARG;
+  if (n_learned > 0 && !learned_offsets) return MSDA_BAD_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  OaeArgs a{};
+  a.feat = f->data;
+  a.C = f->channels;
+  a.cams = f->n_cams;
+  a.L = f->n_levels;
+  a.Q = n_queries;
+  a.shape = f->spatial_shape;
+  a.start = f->scale_start_index;
+  a.anchors = anchors;
+  a.offsets = learned_offsets;
+  a.P = 7 + n_learned;
+  a.K = cams->K;
+  a.R = cams->R;
+  a.T = cams->t;
+  a.strides = strides;
+  a.desc = descriptors;
+  a.vis = visibility;
+  a.memory = memory;
+  a.out = out;
+  a.occluded = all_occluded;
+  a.status = reinterpret_cast<DevStatus*>(workspace);
+  if (cudaMemsetAsync(workspace, 0, sizeof(DevStatus), s) != cudaSuccess) return MSDA_CUDA_ERROR;
+  const uintptr_t al = reinterpret_cast<uintptr_t>(f->data);
+  cudaError_t e;
+  const int C = f->channels;
+  switch (f->dtype) {
+    case MSDA_F32:
+      e = (C % 4 == 0 && al % 16 == 0) ? launch_oae_t<float, 4>(a, s) : launch_oae_t<float, 2>(a, s);
+      break;
+    case MSDA_F16:
+      e = (C % 8 == 0 && al % 16 == 0) ? launch_oae_t<__half, 8>(a, s) : launch_oae_t<__half, 2>(a, s);
+      break;
+    default:
+      e = (C % 8 == 0 && al % 16 == 0) ? launch_oae_t<__nv_bfloat16, 8>(a, s)
+                                       : launch_oae_t<__nv_bfloat16, 2>(a, s);
+  }
+  return e == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
+}
+
+}  // extern "C"

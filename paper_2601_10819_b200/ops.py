@@ -199,3 +199,101 @@ def deformable_aggregation(mc_ms_feat, spatial_shape, scale_start_index, samplin
                           int(bool(normalize)), _ptr(out), _ptr(ws), ws.numel(), _stream(dev))
     _check_call(code, ws, dev, check, "deformable_aggregation")
     return out
+
+
+class Cameras:
+    """Pinhole cameras on device in float64 (CameraModel, geometry.py:56-97)."""
+
+    def __init__(self, K, R, t, device="cuda"):
+        self.K = torch.as_tensor(K, dtype=torch.float64).reshape(-1, 4).to(device).contiguous()
+        self.R = torch.as_tensor(R, dtype=torch.float64).reshape(-1, 9).to(device).contiguous()
+        self.t = torch.as_tensor(t, dtype=torch.float64).reshape(-1, 3).to(device).contiguous()
+        if not (self.K.shape[0] == self.R.shape[0] == self.t.shape[0]):
+            raise ValueError("K, R, t must describe the same number of cameras")
+
+    def descriptor(self) -> L.Cameras:
+        return L.Cameras(_ptr(self.K), _ptr(self.R), _ptr(self.t))
+
+    @classmethod
+    def from_models(cls, cams, device="cuda"):
+        """From objects with focal_x/focal_y/principal_x/principal_y/rotation/translation."""
+        import numpy as np
+
+        K = np.array([[c.focal_x, c.focal_y, c.principal_x, c.principal_y] for c in cams], dtype=np.float64)
+        R = np.array([np.asarray(c.rotation, dtype=np.float64).reshape(9) for c in cams])
+        t = np.array([np.asarray(c.translation, dtype=np.float64).reshape(3) for c in cams])
+        return cls(K, R, t, device)
+
+
+def msda_dense_project(feats: DeviceFeatures, anchors, learned_offsets, cameras: Cameras, strides, weights, dt=0.0,
+                       precision="fast", normalize=False, out=None, check=False):
+    """Dense MSDA with keypoint generation + projection fused into the kernel.
+
+    anchors [bs, Q, 10] (x, y, z, w, l, h, yaw, vx, vy, vz); learned_offsets
+    [n_learned, 3]; strides [L] pixel strides; weights [bs, Q, 7+n_learned,
+    cams, L, G].  Behind-camera keypoints leave the plan.
+    """
+    dev = feats.table.device
+    anchors = anchors.to(device=dev, dtype=torch.float32).contiguous()
+    bs, q_n, ten = anchors.shape
+    if ten != 10 or bs != feats.table.shape[0]:
+        raise ValueError("anchors must be [bs, Q, 10] with bs == feature batch")
+    offs = torch.as_tensor(learned_offsets, dtype=torch.float32).reshape(-1, 3).to(dev).contiguous()
+    n_learned = int(offs.shape[0])
+    p_n = 7 + n_learned
+    strides = torch.as_tensor(strides, dtype=torch.float32).to(dev).contiguous()
+    if strides.numel() != feats.n_levels:
+        raise ValueError("one stride per level")
+    wts = weights.to(device=dev, dtype=torch.float32).contiguous()
+    g_n = int(wts.shape[-1])
+    if tuple(wts.shape) != (bs, q_n, p_n, feats.n_cams, feats.n_levels, g_n):
+        raise ValueError("weights must be [bs, Q, 7 + n_learned, cams, levels, groups]")
+    if cameras.K.shape[0] != feats.n_cams:
+        raise ValueError("camera count differs from the feature table")
+    if out is None:
+        out = torch.empty((bs, q_n, feats.channels), dtype=torch.float32, device=dev)
+    lib = L.lib()
+    nbytes = lib.msda_dense_workspace_size(bs, q_n, p_n, feats.n_cams, feats.n_levels, g_n, feats.channels)
+    ws = WORKSPACE.get(dev, nbytes)
+    fd, cd = feats.descriptor(), cameras.descriptor()
+    code = lib.msda_dense_project(ctypes.byref(fd), q_n, _ptr(anchors), n_learned, _ptr(offs), ctypes.byref(cd),
+                                  _ptr(strides), float(dt), g_n, _ptr(wts), precision_code(precision),
+                                  int(bool(normalize)), _ptr(out), _ptr(ws), ws.numel(), _stream(dev))
+    _check_call(code, ws, dev, check, "msda_dense_project")
+    return out
+
+
+def oae_pool(feats: DeviceFeatures, anchors, learned_offsets, cameras: Cameras, strides, descriptors, visibility,
+             memory, check=True):
+    """Occlusion-aware embedding pooling (oae.py:81-164) for Q queries.
+
+    Returns (embeddings [Q, C] f32 unit-norm, all_occluded [Q] bool).
+    """
+    from .errors import ChannelMismatch
+
+    dev = feats.table.device
+    if feats.table.shape[0] != 1:
+        raise ValueError("oae_pool takes a single-scene feature table")
+    anchors = anchors.to(device=dev, dtype=torch.float32).reshape(-1, 10).contiguous()
+    q_n = int(anchors.shape[0])
+    desc = descriptors.to(device=dev, dtype=torch.float32).contiguous()
+    if desc.dim() != 2 or desc.shape[0] != q_n:
+        raise ValueError("descriptors must be [Q, D]")
+    if desc.shape[1] != feats.channels:
+        raise ChannelMismatch(f"pyramid has C={feats.channels} but descriptor has D={desc.shape[1]}")
+    vis = visibility.to(device=dev, dtype=torch.float32).contiguous()
+    mem = memory.to(device=dev, dtype=torch.float32).contiguous()
+    if tuple(vis.shape) != (q_n, feats.n_cams) or tuple(mem.shape) != (q_n, feats.channels):
+        raise ValueError("visibility must be [Q, cams] and memory [Q, C]")
+    offs = torch.as_tensor(learned_offsets, dtype=torch.float32).reshape(-1, 3).to(dev).contiguous()
+    strides = torch.as_tensor(strides, dtype=torch.float32).to(dev).contiguous()
+    out = torch.empty((q_n, feats.channels), dtype=torch.float32, device=dev)
+    occl = torch.empty((q_n,), dtype=torch.uint8, device=dev)
+    lib = L.lib()
+    ws = WORKSPACE.get(dev, lib.msda_oae_workspace_size(q_n, feats.n_cams, feats.channels))
+    fd, cd = feats.descriptor(), cameras.descriptor()
+    code = lib.msda_oae_pool(ctypes.byref(fd), q_n, _ptr(anchors), int(offs.shape[0]), _ptr(offs), ctypes.byref(cd),
+                             _ptr(strides), _ptr(desc), _ptr(vis), _ptr(mem), _ptr(out), _ptr(occl), _ptr(ws),
+                             ws.numel(), _stream(dev))
+    _check_call(code, ws, dev, check, "oae_pool")
+    return out, occl.bool()

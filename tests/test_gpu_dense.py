@@ -1,0 +1,219 @@
+"""GPU parity of the Sparse4D dense path (deformable_aggregation), the fused
+projection path and OAE pooling.
+
+Oracles: the reference itself (tests/golden/dense.npz, oae.npz) and the
+numpy oracle (oracle/msda_oracle.py) composed as SURVEY §8(c) prescribes.
+Bars: EXACT bitwise; FAST fp32 1e-4 relative (max|d| / max|ref|); f16/bf16
+storage 1e-2 (max|d| / max(1, max|ref|)); projection / OAE (f64 in the
+reference) 1e-4 relative.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import helpers
+from oracle import msda_oracle as mo
+
+pytestmark = pytest.mark.gpu
+
+
+def _feats(ops, torch, grids, shape, dev, dtype=None, batch=1):
+    import torch as _t
+
+    cams, n_levels = shape.shape[:2]
+    table, tiles = mo.pack_grids(grids, cams, n_levels)
+    start = np.array([t[0] for t in tiles], dtype=np.int64).reshape(cams, n_levels)
+    tt = _t.from_numpy(np.ascontiguousarray(np.broadcast_to(table, (batch,) + table.shape))).to(dev)
+    if dtype is not None:
+        tt = tt.to(dtype)
+    return ops.DeviceFeatures(tt.contiguous(), _t.from_numpy(shape), _t.from_numpy(start)), table, tiles
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / max(1e-12, np.abs(b).max()))
+
+
+def test_dense_exact_matches_reference_golden(golden, cuda_dev):
+    import torch
+
+    from paper_2601_10819_b200 import ops
+
+    g = golden("dense")["out"]
+    rng = np.random.default_rng(31)
+    pos = 0
+    for i in range(6):
+        groups = (1, 2, 4)[i % 3]
+        bs = 1 + i % 2
+        grids, shape, loc, wts = helpers.make_dense(rng, bs=bs, n_q=4, n_p=3, cams=2, n_levels=2, groups=groups,
+                                                    channels=8)
+        feats, _, _ = _feats(ops, torch, grids, shape, cuda_dev, batch=bs)
+        for normalize in (False, True):
+            out = ops.deformable_aggregation(feats, None, None, torch.from_numpy(loc).to(cuda_dev),
+                                             torch.from_numpy(wts).to(cuda_dev), precision="exact",
+                                             normalize=normalize, check=True).cpu().numpy().reshape(-1)
+            assert out.tobytes() == g[pos:pos + out.size].tobytes(), (i, normalize)
+            pos += out.size
+
+
+@pytest.mark.parametrize("groups,channels,cams,levels,normalize", [
+    (8, 256, 6, 4, False), (8, 256, 3, 4, True), (1, 64, 2, 3, False), (4, 32, 4, 2, True), (2, 8, 2, 2, False)])
+def test_dense_fast_fp32_tolerance(cuda_dev, groups, channels, cams, levels, normalize):
+    import torch
+
+    from paper_2601_10819_b200 import ops
+
+    rng = np.random.default_rng(100 + groups + channels)
+    grids, shape, loc, wts = helpers.make_dense(rng, bs=2, n_q=7, n_p=13, cams=cams, n_levels=levels, groups=groups,
+                                                channels=channels, size_lo=6, size_hi=30)
+    feats, table, tiles = _feats(ops, torch, grids, shape, cuda_dev, batch=2)
+    t = lambda a: torch.from_numpy(a).to(cuda_dev)  # noqa: E731
+    fast = ops.deformable_aggregation(feats, None, None, t(loc), t(wts), precision="fast", normalize=normalize,
+                                      check=True).cpu().numpy()
+    exact = ops.deformable_aggregation(feats, None, None, t(loc), t(wts), precision="exact", normalize=normalize,
+                                       check=True).cpu().numpy()
+    ref = mo.msda_dense_groups(table, tiles, shape, loc, wts, levels, normalize=normalize)
+    assert exact.tobytes() == ref.tobytes()
+    assert rel(fast, ref) <= 1e-4
+
+
+@pytest.mark.parametrize("dt", ["float16", "bfloat16"])
+def test_dense_fast_half_storage(cuda_dev, dt):
+    import torch
+
+    from paper_2601_10819_b200 import ops
+
+    rng = np.random.default_rng(7)
+    grids, shape, loc, wts = helpers.make_dense(rng, bs=1, n_q=16, n_p=13, cams=6, n_levels=4, groups=8,
+                                                channels=256, size_lo=8, size_hi=40)
+    feats, table, tiles = _feats(ops, torch, grids, shape, cuda_dev, dtype=getattr(torch, dt))
+    t = lambda a: torch.from_numpy(a).to(cuda_dev)  # noqa: E731
+    out = ops.deformable_aggregation(feats, None, None, t(loc), t(wts), check=True).cpu().numpy()
+    ref = mo.msda_dense_groups(table, tiles, shape, loc, wts, 4)
+    assert np.abs(out - ref).max() / max(1.0, np.abs(ref).max()) <= 1e-2
+    rounded = feats.table[0].float().cpu().numpy()
+    ref_r = mo.msda_dense_groups(rounded, tiles, shape, loc, wts, 4)
+    assert rel(out, ref_r) <= 1e-4  # only summation order / FMA differ from the pre-rounded reference
+    ex = ops.deformable_aggregation(feats, None, None, t(loc), t(wts), precision="exact", check=True).cpu().numpy()
+    assert ex.tobytes() == ref_r.tobytes()
+
+
+def _ring(n, radius=12.0, height=4.0, focal=300.0, size=(704, 256)):
+    """camera_looking_at ring (geometry.py:258-290) restated for the test."""
+    Ks, Rs, ts = [], [], []
+    for i in range(n):
+        ang = 2 * math.pi * i / n
+        pos = np.array([radius * math.cos(ang), radius * math.sin(ang), height])
+        fwd = np.array([0.0, 0.0, 0.9]) - pos
+        z = fwd / np.linalg.norm(fwd)
+        x = np.cross(z, [0.0, 0.0, 1.0])
+        x /= np.linalg.norm(x)
+        y = np.cross(z, x)
+        R = np.vstack([x, y, z])
+        Ks.append([focal, focal, size[0] / 2, size[1] / 2])
+        Rs.append(R)
+        ts.append(-R @ pos)
+    return np.array(Ks), np.array(Rs), np.array(ts)
+
+
+def _proj_oracle(table, tiles, anchors, offsets, K, R, T, strides, wts, n_levels, normalize, dt):
+    bs, q_n = anchors.shape[:2]
+    g_n = wts.shape[-1]
+    c_n = table.shape[1]
+    cg = c_n // g_n
+    out = np.zeros((bs * q_n, c_n), dtype=np.float32)
+    cams = list(zip(K, R, T))
+    for b in range(bs):
+        plans = mo.projection_plan(anchors[b].astype(np.float64), offsets.astype(np.float64), cams, strides,
+                                   None, dt=dt)
+        for q, samples in enumerate(plans):
+            for g in range(g_n):
+                pq = [(c, m, np.float32(u), np.float32(v), wts[b, q, p, c, m, g]) for c, m, u, v, p in samples]
+                offs, cam, lvl, uu, vv, ww = mo.csr_from_per_query([pq])
+                sub = np.ascontiguousarray(table[:, g * cg:(g + 1) * cg])
+                if len(pq):
+                    r, _ = mo.msda_exact(sub, tiles, n_levels, offs, cam, lvl, uu, vv, ww, normalize)
+                    out[b * q_n + q, g * cg:(g + 1) * cg] = r[0]
+    return out.reshape(bs, q_n, c_n)
+
+
+@pytest.mark.parametrize("normalize", [False, True])
+def test_dense_project_matches_composed_oracle(cuda_dev, normalize):
+    import torch
+
+    from paper_2601_10819_b200 import ops
+
+    rng = np.random.default_rng(55)
+    cams, n_levels, channels, groups = 4, 4, 64, 4
+    strides = [4.0, 8.0, 16.0, 32.0]
+    grids = {}
+    shape = np.zeros((cams, n_levels, 2), dtype=np.int32)
+    for c in range(cams):
+        for m, s in enumerate(strides):
+            h, w = int(math.ceil(256 / s)), int(math.ceil(704 / s))
+            grids[(c, m)] = rng.uniform(-1, 1, (h, w, channels)).astype(np.float32)
+            shape[c, m] = (h, w)
+    feats, table, tiles = _feats(ops, torch, grids, shape, cuda_dev)
+    K, R, T = _ring(cams)
+    q_n = 24
+    anchors = np.zeros((1, q_n, 10), dtype=np.float32)
+    anchors[0, :, 0:2] = rng.uniform(-4, 4, (q_n, 2))
+    anchors[0, :, 2] = 0.9
+    anchors[0, :, 3:6] = (0.6, 0.6, 1.8)
+    anchors[0, :, 6] = rng.uniform(-math.pi, math.pi, q_n)
+    anchors[0, :, 7:9] = rng.uniform(-1, 1, (q_n, 2))
+    anchors[0, 3, 0:3] = (12.0 * math.cos(0.0), 0.0, 4.5)  # near camera 0: partly behind it
+    offsets = rng.uniform(-1, 1, (6, 3)).astype(np.float32)
+    wts = rng.uniform(0.01, 1.0, (1, q_n, 13, cams, n_levels, groups)).astype(np.float32)
+    camd = ops.Cameras(K, R, T, device=cuda_dev)
+    t = lambda a: torch.from_numpy(a).to(cuda_dev)  # noqa: E731
+    ref = _proj_oracle(table, tiles, anchors, offsets, K, R, T, strides, wts, n_levels, normalize, 0.1)
+    for prec in ("fast", "exact"):
+        out = ops.msda_dense_project(feats, t(anchors), offsets, camd, strides, t(wts), dt=0.1, precision=prec,
+                                     normalize=normalize, check=True).cpu().numpy()
+        assert rel(out, ref) <= 1e-4, prec
+
+
+def test_oae_pool_matches_reference_golden(golden, cuda_dev):
+    import torch
+
+    from paper_2601_10819_b200 import ops
+
+    g = golden("oae")
+    n_cams, n_levels = len(g["K"]), len(g["strides"])
+    grids, pos = {}, 0
+    shape = np.zeros((n_cams, n_levels, 2), dtype=np.int32)
+    for i, (h, w) in enumerate(g["shapes"]):
+        n = h * w * 16
+        grids[(i // n_levels, i % n_levels)] = g["grids"][pos:pos + n].reshape(h, w, 16).astype(np.float32)
+        shape[i // n_levels, i % n_levels] = (h, w)
+        pos += n
+    feats, _, _ = _feats(ops, torch, grids, shape, cuda_dev)
+    camd = ops.Cameras(g["K"], g["R"], g["t"], device=cuda_dev)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(cuda_dev)  # noqa: E731
+    emb, occl = ops.oae_pool(feats, t(g["anchors"].astype(np.float32)), g["offsets"].astype(np.float32), camd,
+                             g["strides"].astype(np.float32), t(g["desc"].astype(np.float32)),
+                             t(g["vis"].astype(np.float32)), t(g["memory"].astype(np.float32)))
+    emb, occl = emb.cpu().numpy(), occl.cpu().numpy()
+    assert list(occl) == [bool(x) for x in g["occluded"]]
+    for q in range(len(emb)):
+        if occl[q]:
+            np.testing.assert_allclose(emb[q], g["memory"][q], rtol=1e-6, atol=1e-7)
+        else:
+            assert np.abs(emb[q] - g["emb"][q]).max() <= 1e-4  # unit vectors: absolute == relative
+
+
+def test_oae_channel_mismatch(cuda_dev):
+    import torch
+
+    from paper_2601_10819_b200 import ops
+    from paper_2601_10819_b200.errors import ChannelMismatch
+
+    rng = np.random.default_rng(3)
+    grids = {(0, 0): rng.standard_normal((8, 8, 4)).astype(np.float32)}
+    feats, _, _ = _feats(ops, torch, grids, np.array([[[8, 8]]], dtype=np.int32), cuda_dev)
+    camd = ops.Cameras([[100, 100, 64, 64]], np.eye(3).reshape(1, 9), [[0, 0, 0]], device=cuda_dev)
+    with pytest.raises(ChannelMismatch):
+        ops.oae_pool(feats, torch.zeros(1, 10), np.zeros((0, 3)), camd, [8.0], torch.zeros(1, 6), torch.ones(1, 1),
+                     torch.zeros(1, 4))
