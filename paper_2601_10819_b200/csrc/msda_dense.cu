@@ -159,7 +159,13 @@ __global__ void __launch_bounds__(kDenseThreads) dense_fast_kernel(DenseArgs a) 
           to_f32<T, VEC>(c[1][k], f1);
           const float cw0 = r0.iw[k] * w0, cw1 = r1.iw[k] * w1;
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) acc[e] = fmaf(f1[e], cw1, fmaf(f0[e], cw0, acc[e]));
+          for (int e = 0; e < VEC; e += 2) {  // FFMA2: two channels per instruction
+            float2 p = __ffma2_rn(make_float2(f0[e], f0[e + 1]), make_float2(cw0, cw0),
+                                  make_float2(acc[e], acc[e + 1]));
+            p = __ffma2_rn(make_float2(f1[e], f1[e + 1]), make_float2(cw1, cw1), p);
+            acc[e] = p.x;
+            acc[e + 1] = p.y;
+          }
         }
       }
       for (; i < n; i += n_split) {
@@ -173,7 +179,12 @@ __global__ void __launch_bounds__(kDenseThreads) dense_fast_kernel(DenseArgs a) 
           to_f32<T, VEC>(ldg_vec<BYTES>(feat + (size_t)r0.row[k] * row_bytes), f0);
           const float cw0 = r0.iw[k] * w0;
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) acc[e] = fmaf(f0[e], cw0, acc[e]);
+          for (int e = 0; e < VEC; e += 2) {
+            const float2 p = __ffma2_rn(make_float2(f0[e], f0[e + 1]), make_float2(cw0, cw0),
+                                        make_float2(acc[e], acc[e + 1]));
+            acc[e] = p.x;
+            acc[e + 1] = p.y;
+          }
         }
       }
     }

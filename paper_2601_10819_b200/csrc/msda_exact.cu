@@ -1,24 +1,37 @@
 // Exact (bit-faithful) MSDA over a CSR sample plan — sm_100a.
 //
 // Two kernels per call:
-//   plan_canon_kernel  one CTA per query: canonical sort of the query's
-//                      samples by (camera, level, v, u, weight)
-//                      (features.py:261-263), sequential f32 weight sum in that
-//                      order (features.py:264-269), then one 32-B SampleRec +
-//                      normalised weight per sample, written back in canonical
-//                      order.  Sort is a bitonic network on 128-bit keys in
-//                      shared memory (global scratch for very long queries).
-//   gather_exact_kernel one thread per (query, VEC-channel slice): walks the
-//                      query's records in canonical order, 16-B vector gathers
-//                      of the four corner rows (channel-last layout), the
-//                      reference f32 expression tree
-//                      ((c00*w00 + c10*w10) + (c01*w01 + c11*w11)) * wn, and a
-//                      sequential f32 accumulate (features.py:219, 271-274).
-//                      Every op is separately rounded (__fmul_rn/__fadd_rn), so
-//                      the output is bit-identical to msda_reference.  The
-//                      EXACT_HALF variant does the same in __half2 with
-//                      __hmul2_rn/__hadd2_rn, i.e. msda_optimized(PACKED_HALF)
-//                      (features.py:306-359).
+//
+//   plan_canon_kernel   one 128-thread CTA per query.  Builds 128-bit keys
+//                       (tile = camera*L + level, v, u, weight) with an
+//                       order-preserving float map, i.e. the canonical order
+//                       of features.py:261-263.  When the query arrives grouped
+//                       by (camera, level) — the reference bench generator and
+//                       every dense expansion do — each sample's canonical
+//                       slot is its run start (binary search) plus its rank in
+//                       the run; otherwise a bitonic sort.  Then the sequential
+//                       f32 weight sum in canonical order (features.py:264-269)
+//                       and one 32-B SampleRec + normalised weight per sample,
+//                       scattered to its canonical slot.
+//
+//   gather_pipe_kernel  one warp per (query, 32*VEC channels): walks the
+//                       query's records in canonical order.  Corner rows
+//                       (channel-last, 16-B per lane, whole 32-B sectors) are
+//                       prefetched D samples ahead with cp.async (LDGSTS,
+//                       zero-fill for out-of-grid corners) into a per-warp
+//                       shared-memory ring; records are staged 32 at a time.
+//                       The reference f32 expression tree
+//                       ((c00*w00 + c10*w10) + (c01*w01 + c11*w11)) * wn and
+//                       the sequential accumulate (features.py:219, 271-274)
+//                       are evaluated two channels per instruction with FFMA2,
+//                       every product and sum separately rounded (the 1.0 and
+//                       -0.0 operands come from kernel parameters so ptxas
+//                       cannot fuse them) — bit-identical to msda_reference.
+//                       The PACKED_HALF variant does the same with
+//                       __hmul2_rn/__hadd2_rn (features.py:306-359).
+//
+//   gather_exact_kernel register-pipelined fallback for channel slices that do
+//                       not span whole warps (small C in tests / odd groups).
 #include <algorithm>
 #include <type_traits>
 
@@ -29,7 +42,11 @@ namespace msda {
 
 namespace {
 
-constexpr int kPlanThreads = 256;
+constexpr int kPlanThreads = 128;
+constexpr int kPlanSmemCap = 1024;  // samples per query canonicalised in shared memory
+constexpr int kRunCap = 256;        // longest (camera, level) run the rank path handles
+
+using u64 = unsigned long long;
 
 struct PlanArgs {
   const int64_t* offsets;
@@ -43,26 +60,22 @@ struct PlanArgs {
   const int32_t* shape;
   const int64_t* start;
   int32_t normalize;
-  int32_t smem_cap;
   int64_t queries_per_batch;  // query q reads batch q / queries_per_batch ...
   int64_t rows_per_batch;     // ... whose table starts rows_per_batch rows later
   SampleRec* rec;
   float* wn;
-  unsigned long long* g_hi;  // global sort scratch [S] (long queries only)
-  unsigned long long* g_lo;
+  u64* g_hi;  // global scratch [S] for queries longer than kPlanSmemCap
+  u64* g_lo;
+  int32_t* g_idx;
   DevStatus* status;
 };
 
-template <typename K>
-__device__ __forceinline__ bool key_gt(K ah, K al, K bh, K bl) {
-  return ah > bh || (ah == bh && al > bl);
-}
+__device__ __forceinline__ bool key_gt(u64 ah, u64 al, u64 bh, u64 bl) { return ah > bh || (ah == bh && al > bl); }
 
 // Always-ascending bitonic network over n keys, virtually padded with +inf to
 // the next power of two (a compare with a padded partner is a no-op, so no
 // padding is ever stored).  j is a power of two: index math is shifts/masks.
-template <typename K>
-__device__ void bitonic_sort(K* hi, K* lo, int n) {
+__device__ void bitonic_sort(u64* hi, u64* lo, int n) {
   int N = 1;
   while (N < n) N <<= 1;
   for (int k = 2; k <= N; k <<= 1) {
@@ -73,7 +86,7 @@ __device__ void bitonic_sort(K* hi, K* lo, int n) {
         const int i = ((t >> lj) << (lj + 1)) | (t & (j - 1));
         const int p = flip ? (i ^ (k - 1)) : (i + j);
         if (p < n) {
-          const K ih = hi[i], il = lo[i], ph = hi[p], pl = lo[p];
+          const u64 ih = hi[i], il = lo[i], ph = hi[p], pl = lo[p];
           if (key_gt(ih, il, ph, pl)) {
             hi[i] = ph;
             lo[i] = pl;
@@ -87,11 +100,8 @@ __device__ void bitonic_sort(K* hi, K* lo, int n) {
   }
 }
 
-constexpr int kRunCap = 128;  // longest (camera, level) run the rank path handles
-
-// first index in [0, n) whose tile (key_hi >> 32) is >= t (keys tile-sorted)
-template <typename K>
-__device__ __forceinline__ int tile_lower_bound(const K* hi, int n, uint32_t t) {
+// first index in [0, n) whose tile (hi >> 32) is >= t; keys tile-sorted
+__device__ __forceinline__ int tile_lower_bound(const u64* hi, int n, uint32_t t) {
   int a = 0, b = n;
   while (a < b) {
     const int m = (a + b) >> 1;
@@ -100,90 +110,88 @@ __device__ __forceinline__ int tile_lower_bound(const K* hi, int n, uint32_t t) 
   return a;
 }
 
-// Canonicalise one query whose keys sit in (khi, klo): sorted keys end up in
-// (shi, slo).  When the samples already arrive grouped by (camera, level) —
-// the reference bench generator and every dense expansion do — each sample's
-// final slot is its run start plus its rank inside the run, computed in
-// parallel; otherwise a bitonic sort.  Returns the sequential f32 weight sum.
-template <typename K>
-__device__ float canon_query(const PlanArgs& a, int64_t q, int n, K* khi, K* klo, K* shi, K* slo, float* s_wsum,
-                             int* s_flag) {
-  // tile-sortedness and longest run
+__device__ __forceinline__ float key_weight(u64 lo) { return unord_f32((uint32_t)(lo & 0xffffffffu)); }
+
+// Canonicalise one query whose n keys sit in (khi, klo).  On return
+// sdst[i] = canonical slot of key i and sw[slot] = its weight; keys are
+// either untouched (rank path) or sorted in place with sdst[i] = i.
+__device__ void canon_slots(int n, u64* khi, u64* klo, int32_t* sdst, float* sw) {
   bool bad = false;
   for (int i = threadIdx.x + 1; i < n; i += blockDim.x) bad |= (khi[i] >> 32) < (khi[i - 1] >> 32);
-  const bool tile_sorted = !__syncthreads_or(bad);
-  bool rank_path = tile_sorted;
-  if (tile_sorted) {
+  bool rank_path = !__syncthreads_or(bad);
+  if (rank_path) {
     bool long_run = false;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      if (i > 0 && (khi[i] >> 32) == (khi[i - 1] >> 32)) continue;  // only run heads probe
-      const uint32_t t = (uint32_t)(khi[i] >> 32);
-      long_run |= (tile_lower_bound(khi, n, t + 1) - i) > kRunCap;
+      if (i > 0 && (khi[i] >> 32) == (khi[i - 1] >> 32)) continue;  // run heads probe their run
+      long_run |= (tile_lower_bound(khi, n, (uint32_t)(khi[i] >> 32) + 1) - i) > kRunCap;
     }
     rank_path = !__syncthreads_or(long_run);
   }
   if (rank_path) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const K ih = khi[i], il = klo[i];
+      const u64 ih = khi[i], il = klo[i];
       const uint32_t t = (uint32_t)(ih >> 32);
       const int rs = tile_lower_bound(khi, n, t);
-      const int re = tile_lower_bound(khi, n, t + 1);
       int rank = 0;
-      for (int j = rs; j < re; ++j) {
-        const K jh = khi[j], jl = klo[j];
+      for (int j = rs; j < n; ++j) {
+        const u64 jh = khi[j];
+        if ((uint32_t)(jh >> 32) != t) break;
+        const u64 jl = klo[j];
         rank += (jh < ih || (jh == ih && (jl < il || (jl == il && j < i)))) ? 1 : 0;
       }
-      shi[rs + rank] = ih;
-      slo[rs + rank] = il;
+      sdst[i] = rs + rank;
+      sw[rs + rank] = key_weight(il);
     }
   } else {
     bitonic_sort(khi, klo, n);
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      shi[i] = khi[i];
-      slo[i] = klo[i];
+      sdst[i] = i;
+      sw[i] = key_weight(klo[i]);
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    float ws = 0.0f;
-    if (a.normalize) {
-      // sequential float32 sum in canonical order (features.py:264-267);
-      // loads run ahead of the dependent add chain
-      int i = 0;
-      for (; i + 4 <= n; i += 4) {
-        const K k0 = slo[i], k1 = slo[i + 1], k2 = slo[i + 2], k3 = slo[i + 3];
-        ws = __fadd_rn(ws, unord_f32((uint32_t)(k0 & 0xffffffffu)));
-        ws = __fadd_rn(ws, unord_f32((uint32_t)(k1 & 0xffffffffu)));
-        ws = __fadd_rn(ws, unord_f32((uint32_t)(k2 & 0xffffffffu)));
-        ws = __fadd_rn(ws, unord_f32((uint32_t)(k3 & 0xffffffffu)));
-      }
-      for (; i < n; ++i) ws = __fadd_rn(ws, unord_f32((uint32_t)(slo[i] & 0xffffffffu)));
-      if (ws == 0.0f) set_status(a.status, MSDA_ZERO_WEIGHT_SUM, q);
+}
+
+// sequential float32 sum in canonical order (features.py:264-267): one
+// thread, loads issued well ahead of the dependent add chain
+__device__ __forceinline__ float sequential_sum(const float* sw, int n, bool vec_ok) {
+  float ws = 0.0f;
+  int i = 0;
+  if (vec_ok) {
+    for (; i + 8 <= n; i += 8) {
+      const float4 a = *reinterpret_cast<const float4*>(sw + i);
+      const float4 b = *reinterpret_cast<const float4*>(sw + i + 4);
+      ws = __fadd_rn(ws, a.x);
+      ws = __fadd_rn(ws, a.y);
+      ws = __fadd_rn(ws, a.z);
+      ws = __fadd_rn(ws, a.w);
+      ws = __fadd_rn(ws, b.x);
+      ws = __fadd_rn(ws, b.y);
+      ws = __fadd_rn(ws, b.z);
+      ws = __fadd_rn(ws, b.w);
     }
-    *s_wsum = ws;
   }
-  __syncthreads();
-  (void)s_flag;
-  return *s_wsum;
+  for (; i < n; ++i) ws = __fadd_rn(ws, sw[i]);
+  return ws;
 }
 
 __global__ void __launch_bounds__(kPlanThreads) plan_canon_kernel(PlanArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  unsigned long long* s_hi = reinterpret_cast<unsigned long long*>(smem_raw);
-  unsigned long long* s_lo = s_hi + a.smem_cap;
-  unsigned long long* s_shi = s_lo + a.smem_cap;
-  unsigned long long* s_slo = s_shi + a.smem_cap;
+  __shared__ __align__(16) u64 s_hi[kPlanSmemCap];
+  __shared__ __align__(16) u64 s_lo[kPlanSmemCap];
+  __shared__ __align__(16) float s_w[kPlanSmemCap];
+  __shared__ __align__(16) int32_t s_dst[kPlanSmemCap];
   __shared__ float s_wsum;
-  __shared__ int s_flag;
   const int n_tiles = a.n_cams * a.n_levels;
 
   for (int64_t q = blockIdx.x; q < a.n_queries; q += gridDim.x) {
     const int64_t lo = a.offsets[q], hi = a.offsets[q + 1];
     const int n = (int)(hi - lo);
     if (n <= 0) continue;
-    const bool in_smem = n <= a.smem_cap;
-    unsigned long long* khi = in_smem ? s_hi : a.g_hi + lo;
-    unsigned long long* klo = in_smem ? s_lo : a.g_lo + lo;
+    const bool in_smem = n <= kPlanSmemCap;
+    u64* khi = in_smem ? s_hi : a.g_hi + lo;
+    u64* klo = in_smem ? s_lo : a.g_lo + lo;
+    float* sw = in_smem ? s_w : a.wn + lo;  // the wn slots double as scratch
+    int32_t* sdst = in_smem ? s_dst : a.g_idx + lo;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const int64_t s = lo + i;
       int c = a.cam[s], l = a.lvl[s];
@@ -194,44 +202,32 @@ __global__ void __launch_bounds__(kPlanThreads) plan_canon_kernel(PlanArgs a) {
         l = 0;
       }
       if (!(isfinite(uu) && isfinite(vv) && isfinite(ww))) set_status(a.status, MSDA_NONFINITE, s);
-      const unsigned long long tile = (unsigned long long)(c * a.n_levels + l);
-      khi[i] = (tile << 32) | ord_f32(vv);
-      klo[i] = ((unsigned long long)ord_f32(uu) << 32) | ord_f32(ww);
+      khi[i] = ((u64)(c * a.n_levels + l) << 32) | ord_f32(vv);
+      klo[i] = ((u64)ord_f32(uu) << 32) | ord_f32(ww);
     }
     __syncthreads();
-    // sorted keys: shared memory, or (long queries) the record area as scratch
-    // — records are written after the keys are consumed, one slot per sample.
-    unsigned long long* shi;
-    unsigned long long* slo;
-    float wsum;
-    if (in_smem) {
-      shi = s_shi;
-      slo = s_slo;
-      wsum = canon_query(a, q, n, s_hi, s_lo, s_shi, s_slo, &s_wsum, &s_flag);
-    } else {
-      shi = reinterpret_cast<unsigned long long*>(a.rec + lo);  // 32 B/sample holds 16 B of key
-      slo = shi + n;
-      wsum = canon_query(a, q, n, khi, klo, shi, slo, &s_wsum, &s_flag);
-      // keys may not live in the record area while records are written:
-      // move them back into the key scratch first
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        khi[i] = shi[i];
-        klo[i] = slo[i];
+    canon_slots(n, khi, klo, sdst, sw);
+    if (threadIdx.x == 0) {
+      float ws = 0.0f;
+      if (a.normalize) {
+        ws = sequential_sum(sw, n, in_smem);
+        if (ws == 0.0f) set_status(a.status, MSDA_ZERO_WEIGHT_SUM, q);
       }
-      __syncthreads();
-      shi = khi;
-      slo = klo;
+      s_wsum = ws;
     }
+    __syncthreads();
+    const float wsum = s_wsum;
     const int64_t row_base = (q / a.queries_per_batch) * a.rows_per_batch;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const unsigned long long kh = shi[i], kl = slo[i];
+      const u64 kh = khi[i], kl = klo[i];
+      const int dst = sdst[i];
       const int t = (int)(kh >> 32);
       const float vv = unord_f32((uint32_t)(kh & 0xffffffffu));
       const float uu = unord_f32((uint32_t)(kl >> 32));
-      const float ww = unord_f32((uint32_t)(kl & 0xffffffffu));
+      const float ww = key_weight(kl);
       const int tt = t < n_tiles ? t : 0;
-      a.rec[lo + i] = make_record(uu, vv, row_base + a.start[tt], a.shape[2 * tt], a.shape[2 * tt + 1]);
-      a.wn[lo + i] = a.normalize ? __fdiv_rn(ww, wsum) : ww;
+      a.rec[lo + dst] = make_record(uu, vv, row_base + a.start[tt], a.shape[2 * tt], a.shape[2 * tt + 1]);
+      a.wn[lo + dst] = a.normalize ? __fdiv_rn(ww, wsum) : ww;
     }
     __syncthreads();
   }
@@ -242,16 +238,18 @@ __global__ void __launch_bounds__(kPlanThreads) plan_canon_kernel(PlanArgs a) {
 
 struct GatherArgs {
   const void* feat;
-  int32_t C;          // channels processed (slice width)
-  int32_t row_elems;  // elements per feature row (full C)
-  int32_t c_off;      // first channel of the slice
-  int32_t out_stride; // floats per output row
+  int32_t C;           // channels processed (slice width)
+  int32_t row_elems;   // elements per feature row (full C)
+  int32_t c_off;       // first channel of the slice
+  int32_t out_stride;  // floats per output row
   int64_t n_queries;
   const int64_t* offsets;
   const SampleRec* rec;
   const float* wn;
   float* out;
   uint8_t* empty;
+  float2 one2;  // (1, 1)   — FFMA2 operands that make exact adds / products;
+  float2 nz2;   // (-0, -0)   passed as parameters so ptxas cannot fuse them
 };
 
 __device__ __forceinline__ SampleRec ld_rec(const SampleRec* p) {
@@ -263,6 +261,49 @@ __device__ __forceinline__ SampleRec ld_rec(const SampleRec* p) {
                : "=f"(r.iw[0]), "=f"(r.iw[1]), "=f"(r.iw[2]), "=f"(r.iw[3])
                : "l"(reinterpret_cast<const char*>(p) + 16));
   return r;
+}
+
+// acc[e] += wn * ((c0*w0 + c1*w1) + (c2*w2 + c3*w3)), two channels per FFMA2,
+// every product and sum rounded once (x*y + -0 == round(x*y); x*1 + y ==
+// round(x + y)).
+template <int VEC>
+__device__ __forceinline__ void exact_accumulate(float* acc, const float (*c)[VEC], const float4 iw, const float wn,
+                                                 const float2 one2, const float2 nz2) {
+  static_assert(VEC % 2 == 0, "pairs");
+  const float2 w0 = make_float2(iw.x, iw.x), w1 = make_float2(iw.y, iw.y);
+  const float2 w2 = make_float2(iw.z, iw.z), w3 = make_float2(iw.w, iw.w);
+  const float2 ws = make_float2(wn, wn);
+#pragma unroll
+  for (int e = 0; e < VEC; e += 2) {
+    const float2 a = __ffma2_rn(make_float2(c[0][e], c[0][e + 1]), w0, nz2);
+    const float2 b = __ffma2_rn(make_float2(c[1][e], c[1][e + 1]), w1, nz2);
+    const float2 d = __ffma2_rn(make_float2(c[2][e], c[2][e + 1]), w2, nz2);
+    const float2 f = __ffma2_rn(make_float2(c[3][e], c[3][e + 1]), w3, nz2);
+    const float2 ab = __ffma2_rn(a, one2, b);
+    const float2 df = __ffma2_rn(d, one2, f);
+    const float2 t = __ffma2_rn(ab, one2, df);
+    const float2 tw = __ffma2_rn(t, ws, nz2);
+    const float2 r = __ffma2_rn(tw, one2, make_float2(acc[e], acc[e + 1]));
+    acc[e] = r.x;
+    acc[e + 1] = r.y;
+  }
+}
+
+template <int VEC>
+__device__ __forceinline__ void half_accumulate(__half2* acch, const void* const* cvp, const float4 iw, const float wn) {
+  const __half2 hw0 = __float2half2_rn(iw.x), hw1 = __float2half2_rn(iw.y);
+  const __half2 hw2 = __float2half2_rn(iw.z), hw3 = __float2half2_rn(iw.w);
+  const __half2 hs = __float2half2_rn(wn);
+  const __half2* h0 = reinterpret_cast<const __half2*>(cvp[0]);
+  const __half2* h1 = reinterpret_cast<const __half2*>(cvp[1]);
+  const __half2* h2 = reinterpret_cast<const __half2*>(cvp[2]);
+  const __half2* h3 = reinterpret_cast<const __half2*>(cvp[3]);
+#pragma unroll
+  for (int e = 0; e < VEC / 2; ++e) {
+    const __half2 t = __hadd2_rn(__hadd2_rn(__hmul2_rn(h0[e], hw0), __hmul2_rn(h1[e], hw1)),
+                                 __hadd2_rn(__hmul2_rn(h2[e], hw2), __hmul2_rn(h3[e], hw3)));
+    acch[e] = __hadd2_rn(acch[e], __hmul2_rn(t, hs));
+  }
 }
 
 // T: storage type; VEC: channels per thread; HALF: f16 arithmetic.
@@ -279,14 +320,13 @@ __global__ void __launch_bounds__(256) gather_exact_kernel(GatherArgs a) {
   const size_t row_bytes = (size_t)a.row_elems * sizeof(T);
 
   float accf[VEC];
-  __half2 acch[VEC / 2 > 0 ? VEC / 2 : 1];
+  __half2 acch[VEC / 2];
 #pragma unroll
   for (int e = 0; e < VEC; ++e) accf[e] = 0.0f;
 #pragma unroll
-  for (int e = 0; e < (VEC / 2 > 0 ? VEC / 2 : 1); ++e) acch[e] = __float2half2_rn(0.0f);
+  for (int e = 0; e < VEC / 2; ++e) acch[e] = __float2half2_rn(0.0f);
 
-  int64_t i = lo;
-  for (; i < hi; i += UNROLL) {
+  for (int64_t i = lo; i < hi; i += UNROLL) {
     SampleRec r[UNROLL];
     float s[UNROLL];
     RawVec<BYTES> cv[UNROLL][4];
@@ -302,41 +342,22 @@ __global__ void __launch_bounds__(256) gather_exact_kernel(GatherArgs a) {
       }
     }
 #pragma unroll
-    for (int j = 0; j < UNROLL; ++j) {
+    for (int j = 0; j < UNROLL; ++j)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < 4; ++k)
         cv[j][k] = (r[j].row[k] >= 0) ? ldg_vec<BYTES>(feat + (size_t)r[j].row[k] * row_bytes) : zero_vec<BYTES>();
-      }
-    }
 #pragma unroll
     for (int j = 0; j < UNROLL; ++j) {
       if (i + j >= hi) break;
+      const float4 iw = make_float4(r[j].iw[0], r[j].iw[1], r[j].iw[2], r[j].iw[3]);
       if constexpr (!HALF) {
         float c[4][VEC];
 #pragma unroll
         for (int k = 0; k < 4; ++k) to_f32<T, VEC>(cv[j][k], c[k]);
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          const float t = __fadd_rn(__fadd_rn(__fmul_rn(c[0][e], r[j].iw[0]), __fmul_rn(c[1][e], r[j].iw[1])),
-                                    __fadd_rn(__fmul_rn(c[2][e], r[j].iw[2]), __fmul_rn(c[3][e], r[j].iw[3])));
-          accf[e] = __fadd_rn(accf[e], __fmul_rn(s[j], t));
-        }
+        exact_accumulate<VEC>(accf, c, iw, s[j], a.one2, a.nz2);
       } else {
-        const __half2 hw0 = __float2half2_rn(r[j].iw[0]);
-        const __half2 hw1 = __float2half2_rn(r[j].iw[1]);
-        const __half2 hw2 = __float2half2_rn(r[j].iw[2]);
-        const __half2 hw3 = __float2half2_rn(r[j].iw[3]);
-        const __half2 hs = __float2half2_rn(s[j]);
-        const __half2* h0 = reinterpret_cast<const __half2*>(&cv[j][0]);
-        const __half2* h1 = reinterpret_cast<const __half2*>(&cv[j][1]);
-        const __half2* h2 = reinterpret_cast<const __half2*>(&cv[j][2]);
-        const __half2* h3 = reinterpret_cast<const __half2*>(&cv[j][3]);
-#pragma unroll
-        for (int e = 0; e < VEC / 2; ++e) {
-          const __half2 t = __hadd2_rn(__hadd2_rn(__hmul2_rn(h0[e], hw0), __hmul2_rn(h1[e], hw1)),
-                                       __hadd2_rn(__hmul2_rn(h2[e], hw2), __hmul2_rn(h3[e], hw3)));
-          acch[e] = __hadd2_rn(acch[e], __hmul2_rn(t, hs));
-        }
+        const void* cvp[4] = {&cv[j][0], &cv[j][1], &cv[j][2], &cv[j][3]};
+        half_accumulate<VEC>(acch, cvp, iw, s[j]);
       }
     }
   }
@@ -360,11 +381,10 @@ __global__ void __launch_bounds__(256) gather_exact_kernel(GatherArgs a) {
 // Pipelined gather (the production path when a query's channel slice spans
 // whole warps).  Same arithmetic and order as gather_exact_kernel; the
 // difference is memory-level parallelism: each lane keeps D samples' corner
-// rows in flight with cp.async (LDGSTS, zero-fill for out-of-grid corners)
-// into a per-warp shared-memory ring, and the query's records are staged 32 at
-// a time in shared memory (one coalesced load per lane, read back as warp
-// broadcasts), fetched one batch ahead.  Registers stay low, so the ring depth
-// — not the register file — sets the bytes in flight per SM.
+// rows in flight with cp.async into a per-warp shared-memory ring, and the
+// query's records are staged 32 at a time (one coalesced load per lane, read
+// back as warp broadcasts), fetched one batch ahead.  Registers stay low, so
+// the ring depth — not the register file — sets the bytes in flight per SM.
 
 template <int BYTES>
 __device__ __forceinline__ void cp_async_zfill(uint32_t dst, const void* src, bool valid) {
@@ -383,10 +403,11 @@ __device__ __forceinline__ void cp_async_wait() {
 
 template <int BYTES, int D>
 struct PipeSmem {
-  static constexpr int kCorner = D * 4 * 32 * BYTES;        // corner ring
-  static constexpr int kRows = 2 * 32 * 16;                 // int4 rows[2][32]
-  static constexpr int kIw = 2 * 32 * 16;                   // float4 iw[2][32]
-  static constexpr int kWn = 2 * 32 * 4;                    // float wn[2][32]
+  static constexpr int kSlot = 4 * 32 * BYTES;  // one sample: 4 corners x 32 lanes
+  static constexpr int kCorner = D * kSlot;      // corner ring
+  static constexpr int kRows = 2 * 32 * 16;      // int4 rows[2][32]
+  static constexpr int kIw = 2 * 32 * 16;        // float4 iw[2][32]
+  static constexpr int kWn = 2 * 32 * 4;         // float wn[2][32]
   static constexpr int kPerWarp = kCorner + kRows + kIw + kWn;
 };
 
@@ -403,28 +424,31 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   float4* s_iw = reinterpret_cast<float4*>(base + SM::kCorner + SM::kRows);
   float* s_wn = reinterpret_cast<float*>(base + SM::kCorner + SM::kRows + SM::kIw);
   const uint32_t ring = (uint32_t)__cvta_generic_to_shared(base) + lane * BYTES;
+  const unsigned char* ring_ptr = base + lane * BYTES;
 
   const int warps_per_q = a.C / VEC / 32;
   const int64_t gw = (int64_t)blockIdx.x * kPipeWarps + warp;
   const int64_t q = gw / warps_per_q;
   if (q >= a.n_queries) return;
   const int c0 = (int)(gw - q * warps_per_q) * 32 * VEC + lane * VEC;
-  const int64_t lo = a.offsets[q], hi = a.offsets[q + 1];
-  const int64_t n = hi - lo;
+  const int64_t lo = a.offsets[q];
+  const int n = (int)(a.offsets[q + 1] - lo);
+  const SampleRec* rec = a.rec + lo;
+  const float* wnp = a.wn + lo;
   const char* featc = reinterpret_cast<const char*>(a.feat) + (size_t)(a.c_off + c0) * sizeof(T);
-  const size_t row_bytes = (size_t)a.row_elems * sizeof(T);
+  const uint32_t row_bytes = (uint32_t)a.row_elems * (uint32_t)sizeof(T);
 
-  // record batch b: lane j holds sample lo + 32 b + j
+  // record batch b: lane j holds sample 32 b + j
   int4 r_rows = make_int4(-1, -1, -1, -1);
   float4 r_iw = make_float4(0.f, 0.f, 0.f, 0.f);
   float r_wn = 0.0f;
-  auto load_batch = [&](int64_t b) {
-    const int64_t s = lo + b * 32 + lane;
-    if (s < hi) {
-      const SampleRec r = ld_rec(a.rec + s);
+  auto load_batch = [&](int b) {
+    const int s = b * 32 + lane;
+    if (s < n) {
+      const SampleRec r = ld_rec(rec + s);
       r_rows = make_int4(r.row[0], r.row[1], r.row[2], r.row[3]);
       r_iw = make_float4(r.iw[0], r.iw[1], r.iw[2], r.iw[3]);
-      r_wn = __ldg(a.wn + s);
+      r_wn = __ldg(wnp + s);
     }
   };
   auto store_batch = [&](int buf) {
@@ -432,14 +456,14 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
     s_iw[buf * 32 + lane] = r_iw;
     s_wn[buf * 32 + lane] = r_wn;
   };
-  auto issue = [&](int64_t k) {
-    const int buf = (int)((k >> 5) & 1), j = (int)(k & 31);
-    const int4 rows = s_rows[buf * 32 + j];
-    const uint32_t dst = ring + (uint32_t)((k % D) * 4 * 32 * BYTES);
-    cp_async_zfill<BYTES>(dst, rows.x >= 0 ? featc + (size_t)rows.x * row_bytes : featc, rows.x >= 0);
-    cp_async_zfill<BYTES>(dst + 32 * BYTES, rows.y >= 0 ? featc + (size_t)rows.y * row_bytes : featc, rows.y >= 0);
-    cp_async_zfill<BYTES>(dst + 64 * BYTES, rows.z >= 0 ? featc + (size_t)rows.z * row_bytes : featc, rows.z >= 0);
-    cp_async_zfill<BYTES>(dst + 96 * BYTES, rows.w >= 0 ? featc + (size_t)rows.w * row_bytes : featc, rows.w >= 0);
+  auto issue = [&](int k, uint32_t slot_off) {
+    const int4 rows = s_rows[((k >> 5) & 1) * 32 + (k & 31)];
+    const uint32_t dst = ring + slot_off;
+    const int r0 = max(rows.x, 0), r1 = max(rows.y, 0), r2 = max(rows.z, 0), r3 = max(rows.w, 0);
+    cp_async_zfill<BYTES>(dst, featc + (size_t)r0 * row_bytes, rows.x >= 0);
+    cp_async_zfill<BYTES>(dst + 32 * BYTES, featc + (size_t)r1 * row_bytes, rows.y >= 0);
+    cp_async_zfill<BYTES>(dst + 64 * BYTES, featc + (size_t)r2 * row_bytes, rows.z >= 0);
+    cp_async_zfill<BYTES>(dst + 96 * BYTES, featc + (size_t)r3 * row_bytes, rows.w >= 0);
   };
 
   load_batch(0);
@@ -448,23 +472,24 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   load_batch(1);
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    if (k < n) issue(k);
+    if (k < n) issue(k, (uint32_t)(k * SM::kSlot));
     cp_async_commit();
   }
+  uint32_t read_off = 0;
 
   float accf[VEC];
-  __half2 acch[VEC / 2 > 0 ? VEC / 2 : 1];
+  __half2 acch[VEC / 2];
 #pragma unroll
   for (int e = 0; e < VEC; ++e) accf[e] = 0.0f;
 #pragma unroll
-  for (int e = 0; e < (VEC / 2 > 0 ? VEC / 2 : 1); ++e) acch[e] = __float2half2_rn(0.0f);
+  for (int e = 0; e < VEC / 2; ++e) acch[e] = __float2half2_rn(0.0f);
 
-  for (int64_t i = 0; i < n; ++i) {
+  for (int i = 0; i < n; ++i) {
     cp_async_wait<D - 1>();
-    const int buf = (int)((i >> 5) & 1), j = (int)(i & 31);
-    const float4 iw = s_iw[buf * 32 + j];
-    const float wn = s_wn[buf * 32 + j];
-    const unsigned char* src = base + (size_t)((i % D) * 4 * 32 + lane) * BYTES;
+    const int bi = ((i >> 5) & 1) * 32 + (i & 31);
+    const float4 iw = s_iw[bi];
+    const float wn = s_wn[bi];
+    const unsigned char* src = ring_ptr + read_off;
     RawVec<BYTES> cv[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) cv[k] = *reinterpret_cast<const RawVec<BYTES>*>(src + k * 32 * BYTES);
@@ -472,45 +497,37 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
       float c[4][VEC];
 #pragma unroll
       for (int k = 0; k < 4; ++k) to_f32<T, VEC>(cv[k], c[k]);
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) {
-        const float t = __fadd_rn(__fadd_rn(__fmul_rn(c[0][e], iw.x), __fmul_rn(c[1][e], iw.y)),
-                                  __fadd_rn(__fmul_rn(c[2][e], iw.z), __fmul_rn(c[3][e], iw.w)));
-        accf[e] = __fadd_rn(accf[e], __fmul_rn(wn, t));
-      }
+      exact_accumulate<VEC>(accf, c, iw, wn, a.one2, a.nz2);
     } else {
-      const __half2 hw0 = __float2half2_rn(iw.x), hw1 = __float2half2_rn(iw.y);
-      const __half2 hw2 = __float2half2_rn(iw.z), hw3 = __float2half2_rn(iw.w);
-      const __half2 hs = __float2half2_rn(wn);
-      const __half2* h0 = reinterpret_cast<const __half2*>(&cv[0]);
-      const __half2* h1 = reinterpret_cast<const __half2*>(&cv[1]);
-      const __half2* h2 = reinterpret_cast<const __half2*>(&cv[2]);
-      const __half2* h3 = reinterpret_cast<const __half2*>(&cv[3]);
-#pragma unroll
-      for (int e = 0; e < VEC / 2; ++e) {
-        const __half2 t = __hadd2_rn(__hadd2_rn(__hmul2_rn(h0[e], hw0), __hmul2_rn(h1[e], hw1)),
-                                     __hadd2_rn(__hmul2_rn(h2[e], hw2), __hmul2_rn(h3[e], hw3)));
-        acch[e] = __hadd2_rn(acch[e], __hmul2_rn(t, hs));
-      }
+      const void* cvp[4] = {&cv[0], &cv[1], &cv[2], &cv[3]};
+      half_accumulate<VEC>(acch, cvp, iw, wn);
     }
-    const int64_t k = i + D;
+    const int k = i + D;
     if (k < n) {
       if ((k & 31) == 0) {  // entering record batch k/32: publish it, prefetch the next
         __syncwarp();
-        store_batch((int)((k >> 5) & 1));
+        store_batch((k >> 5) & 1);
         __syncwarp();
         load_batch((k >> 5) + 1);
       }
-      issue(k);
+      issue(k, read_off);  // the slot of sample i (just consumed) takes sample i + D
     }
     cp_async_commit();
+    read_off += SM::kSlot;
+    if (read_off == (uint32_t)SM::kCorner) read_off = 0;
   }
   cp_async_wait<0>();
 
   float* o = a.out + q * a.out_stride + a.c_off + c0;
   if constexpr (!HALF) {
+    if constexpr (VEC % 4 == 0) {
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) o[e] = accf[e];
+      for (int e = 0; e < VEC; e += 4)
+        *reinterpret_cast<float4*>(o + e) = make_float4(accf[e], accf[e + 1], accf[e + 2], accf[e + 3]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) o[e] = accf[e];
+    }
   } else {
 #pragma unroll
     for (int e = 0; e < VEC / 2; ++e) {
@@ -526,7 +543,7 @@ template <typename T, int VEC, bool HALF, int D>
 cudaError_t launch_gather_pipe(const GatherArgs& g, cudaStream_t stream) {
   constexpr int BYTES = VEC * (int)sizeof(T);
   const int smem = kPipeWarps * PipeSmem<BYTES, D>::kPerWarp;
-  static bool attr_set = false;  // per instantiation; benign race (idempotent)
+  static bool attr_set = false;  // per instantiation; idempotent
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(gather_pipe_kernel<T, VEC, HALF, D>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -562,7 +579,8 @@ size_t exact_workspace_bytes(int64_t n_queries, int64_t n_samples) {
   size_t b = kStatusBytes;
   b += align_up((size_t)n_samples * sizeof(SampleRec), 256);
   b += align_up((size_t)n_samples * sizeof(float), 256);
-  b += 2 * align_up((size_t)n_samples * sizeof(unsigned long long), 256);
+  b += 2 * align_up((size_t)n_samples * sizeof(u64), 256);
+  b += align_up((size_t)n_samples * sizeof(int32_t), 256);
   return b;
 }
 
@@ -575,9 +593,11 @@ ExactWorkspace carve_exact_workspace(void* ws, int64_t n_samples) {
   p += align_up((size_t)n_samples * sizeof(SampleRec), 256);
   w.wn = reinterpret_cast<float*>(p);
   p += align_up((size_t)n_samples * sizeof(float), 256);
-  w.g_hi = reinterpret_cast<unsigned long long*>(p);
-  p += align_up((size_t)n_samples * sizeof(unsigned long long), 256);
-  w.g_lo = reinterpret_cast<unsigned long long*>(p);
+  w.g_hi = reinterpret_cast<u64*>(p);
+  p += align_up((size_t)n_samples * sizeof(u64), 256);
+  w.g_lo = reinterpret_cast<u64*>(p);
+  p += align_up((size_t)n_samples * sizeof(u64), 256);
+  w.g_idx = reinterpret_cast<int32_t*>(p);
   return w;
 }
 
@@ -598,17 +618,17 @@ cudaError_t launch_plan_canon(const msda_features_t& f, const msda_csr_plan_t& p
   a.shape = f.spatial_shape;
   a.start = f.scale_start_index;
   a.normalize = normalize;
-  a.smem_cap = 1024;  // 32 KB of keys (unsorted + sorted) per CTA; longer queries use global scratch
   a.queries_per_batch = queries_per_batch > 0 ? queries_per_batch : (p.n_queries > 0 ? p.n_queries : 1);
   a.rows_per_batch = f.n_rows;
   a.rec = w.rec;
   a.wn = w.wn;
   a.g_hi = w.g_hi;
   a.g_lo = w.g_lo;
+  a.g_idx = w.g_idx;
   a.status = w.status;
-  const size_t smem = (size_t)a.smem_cap * 4 * sizeof(unsigned long long);
-  const int64_t grid = std::min<int64_t>(p.n_queries, (int64_t)num_sms * 16);
-  plan_canon_kernel<<<(unsigned)grid, kPlanThreads, smem, stream>>>(a);
+  // one CTA per query while they all fit on the device at once
+  const int64_t grid = std::min<int64_t>(p.n_queries, (int64_t)num_sms * 8);
+  plan_canon_kernel<<<(unsigned)grid, kPlanThreads, 0, stream>>>(a);
   return cudaGetLastError();
 }
 
@@ -631,9 +651,12 @@ cudaError_t launch_gather_exact(const msda_features_t& f, const msda_csr_plan_t&
   g.wn = w.wn;
   g.out = out;
   g.empty = empty;
+  g.one2 = make_float2(1.0f, 1.0f);
+  g.nz2 = make_float2(-0.0f, -0.0f);
   const size_t esz = f.dtype == MSDA_F32 ? 4 : 2;
-  // vector width must divide the slice and keep every row access aligned
+  // vector width must divide the slice and keep every row (and output) access aligned
   const uintptr_t base = reinterpret_cast<uintptr_t>(f.data) | ((size_t)c_off * esz) | ((size_t)f.channels * esz);
+  const uintptr_t obase = reinterpret_cast<uintptr_t>(out) | ((size_t)c_off * 4) | ((size_t)f.channels * 4);
   const int C = c_count;
   if (precision == MSDA_EXACT_HALF) {
     if (C % 128 == 0 && base % 8 == 0) return launch_gather<__half, 4, true>(g, stream);
@@ -643,8 +666,7 @@ cudaError_t launch_gather_exact(const msda_features_t& f, const msda_csr_plan_t&
   }
   switch (f.dtype) {
     case MSDA_F32:
-      if (C % 4 == 0 && base % 16 == 0) return launch_gather<float, 4, false>(g, stream);
-      if (C % 64 == 0 && base % 8 == 0) return launch_gather<float, 2, false>(g, stream);
+      if (C % 4 == 0 && base % 16 == 0 && obase % 16 == 0) return launch_gather<float, 4, false>(g, stream);
       return launch_gather<float, 2, false>(g, stream);
     case MSDA_F16:
       if (C % 128 == 0 && base % 8 == 0) return launch_gather<__half, 4, false>(g, stream);

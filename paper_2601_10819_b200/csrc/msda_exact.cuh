@@ -10,6 +10,7 @@ struct ExactWorkspace {
   float* wn;
   unsigned long long* g_hi;
   unsigned long long* g_lo;
+  int32_t* g_idx;
 };
 
 size_t exact_workspace_bytes(int64_t n_queries, int64_t n_samples);

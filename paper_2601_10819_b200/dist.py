@@ -1,0 +1,113 @@
+"""Multi-GPU drivers: one process per GPU, torch.distributed for the plumbing.
+
+Two partitionings:
+
+* **Stream-sharded** (``shard_streams``): independent camera-stream batches
+  (scenes) are dealt round-robin to ranks; each rank owns its scenes'
+  features, anchors and weights end to end.  No data-path collective.
+* **Camera-sharded** (``CameraShardedAggregation``): one scene's cameras are
+  split into contiguous ranges, each rank aggregates over its own cameras
+  (un-normalised partial numerator ``[bs, Q, C]`` plus, when normalising,
+  the partial per-(anchor, group) weight sums ``[bs, Q, G]``), and the
+  partials are summed with one all-reduce (NCCL over NVLink on GPUs; any
+  backend works).  The cross-rank summation order differs from the
+  reference's sequential order, so this mode is tolerance parity only.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+
+def camera_range(n_cams: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced camera range [lo, hi) of ``rank``."""
+    base, extra = divmod(n_cams, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def shard_streams(n_scenes: int, rank: int, world: int) -> list[int]:
+    """Scenes (independent stream batches) owned by ``rank``, round-robin."""
+    return list(range(rank, n_scenes, world))
+
+
+@dataclass
+class CameraShardedAggregation:
+    """Sparse4D deformable aggregation of one scene with cameras across ranks.
+
+    ``local_fn(loc, weights)`` aggregates this rank's cameras with
+    ``normalize=False`` and returns ``[bs, Q, C]`` float32 on the rank's
+    device; on GPUs it is ``ops.deformable_aggregation`` bound to the rank's
+    feature table (see :meth:`for_device_features`).
+    """
+
+    n_cams: int
+    local_fn: Callable
+    group: object = None
+
+    def __post_init__(self):
+        self.rank = dist.get_rank(self.group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(self.group) if dist.is_initialized() else 1
+        self.cam_lo, self.cam_hi = camera_range(self.n_cams, self.rank, self.world)
+
+    def __call__(self, sampling_location, weights, normalize: bool = False):
+        """sampling_location [bs, Q, P, cams, 2], weights [bs, Q, P, cams, L, G]
+        for ALL cameras (each rank slices its own); returns [bs, Q, C]."""
+        loc = sampling_location[:, :, :, self.cam_lo:self.cam_hi].contiguous()
+        wts = weights[:, :, :, self.cam_lo:self.cam_hi].contiguous()
+        part = self.local_fn(loc, wts)
+        bs, q_n, c_n = part.shape
+        g_n = weights.shape[-1]
+        if normalize:
+            wsum = wts.sum(dim=(2, 3, 4), dtype=torch.float32).to(part.device)  # [bs, Q, G]
+            buf = torch.cat([part.reshape(bs * q_n, c_n), wsum.reshape(bs * q_n, g_n)], dim=1)
+        else:
+            buf = part.reshape(bs * q_n, c_n)
+        if self.world > 1:
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
+        out = buf[:, :c_n].reshape(bs, q_n, c_n)
+        if normalize:
+            ws = buf[:, c_n:].reshape(bs, q_n, g_n)
+            if bool((ws == 0).any()):
+                raise ValueError("an anchor's weights sum to zero, cannot renormalize")
+            out = (out.reshape(bs, q_n, g_n, c_n // g_n) / ws.unsqueeze(-1)).reshape(bs, q_n, c_n)
+        return out
+
+    @classmethod
+    def for_device_features(cls, n_cams, local_feats, precision="fast", group=None):
+        """Bind to this rank's ``ops.DeviceFeatures`` (its camera range only)."""
+        from . import ops
+
+        def local(loc, wts):
+            return ops.deformable_aggregation(local_feats, None, None, loc, wts, precision=precision,
+                                              normalize=False)
+
+        return cls(n_cams, local, group)
+
+
+def init_from_env(backend: str | None = None):
+    """Initialise the default process group from torchrun's environment.
+
+    Uses NCCL with the rank's GPU when CUDA is available, gloo otherwise.
+    """
+    import os
+
+    if dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29511")
+    if backend is None:
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+    if backend == "nccl":
+        local = int(os.environ.get("LOCAL_RANK", 0))
+        torch.cuda.set_device(local)
+        dist.init_process_group(backend, rank=rank, world_size=world, device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend, rank=rank, world_size=world)
+    return rank, world

@@ -1,0 +1,214 @@
+#!/usr/bin/env python
+"""Per-path GPU timings for the non-headline BASELINE configs (dense Sparse4D
+API, fused projection, OAE pooling).  bench.py holds the driver contract; this
+tool prints one JSON line per config for DESIGN.md / profiles/.
+
+Synthetic inputs per SURVEY §8(d): features U[-1, 1) channel-last,
+sampling_location U[0, 1)^2 per (b, q, p, cam) shared across levels, weights
+softmax over (P*cams*L) of N(0, 1) logits per (b, q, g), G = 8.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import sys
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2601_10819_b200 import ops  # noqa: E402
+
+CFG1_LEVELS = [(64, 176), (32, 88), (16, 44), (8, 22)]
+CFG2_LEVELS = [(270, 480), (135, 240), (68, 120), (34, 60)]
+L2 = 126 * 1024 * 1024
+
+
+def peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    return json.loads(p.read_text())["hbm_gbs"] if p.exists() else 6650.0
+
+
+def make_feats(cams, levels, C, dtype, dev, bs=1):
+    rows = cams * sum(h * w for h, w in levels)
+    g = torch.Generator(device=dev).manual_seed(0)
+    table = (torch.rand((bs, rows, C), generator=g, device=dev) * 2 - 1).to(dtype)
+    shape = torch.tensor([[list(l) for l in levels]] * cams, dtype=torch.int32)
+    start, r = [], 0
+    for _ in range(cams):
+        s = []
+        for h, w in levels:
+            s.append(r)
+            r += h * w
+        start.append(s)
+    return ops.DeviceFeatures(table, shape, torch.tensor(start, dtype=torch.int64))
+
+
+def make_dense_inputs(bs, Q, P, cams, L, G, dev):
+    g = torch.Generator(device=dev).manual_seed(1)
+    loc = torch.rand((bs, Q, P, cams, 2), generator=g, device=dev)
+    logits = torch.randn((bs, Q, P * cams * L, G), generator=g, device=dev)
+    w = torch.softmax(logits, dim=2).reshape(bs, Q, P, cams, L, G).contiguous()
+    return loc, w
+
+
+def touched_bytes(feats, loc, esize):
+    """Unique in-bounds corner cells of the dense sampling."""
+    shape = feats.spatial_shape.long()
+    start = feats.scale_start_index
+    bs, Q, P, cams, _ = loc.shape
+    L = shape.shape[1]
+    idx = []
+    for c in range(cams):
+        for m in range(L):
+            H, W = int(shape[c, m, 0]), int(shape[c, m, 1])
+            u = loc[:, :, :, c, 0] * W - 0.5
+            v = loc[:, :, :, c, 1] * H - 0.5
+            x0, y0 = torch.floor(u).long(), torch.floor(v).long()
+            for dy in (0, 1):
+                for dx in (0, 1):
+                    x, y = x0 + dx, y0 + dy
+                    ok = (x >= 0) & (x < W) & (y >= 0) & (y < H)
+                    b = torch.arange(bs, device=loc.device).view(bs, 1, 1).expand_as(x)
+                    idx.append((b * feats.table.shape[1] + int(start[c, m]) + y * W + x)[ok])
+    return torch.unique(torch.cat(idx)).numel() * feats.channels * esize
+
+
+def time_fn(fn, reps, flush):
+    scratch = torch.empty(2 * L2 // 4, device="cuda") if flush else None
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        if flush:
+            scratch.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ts.sort()
+    return ts[len(ts) // 2], ts[0]
+
+
+def dense_case(name, cams, levels, C, G, dtype, precision, reps, dev, Q=900, P=13, bs=1):
+    feats = make_feats(cams, levels, C, dtype, dev, bs)
+    loc, w = make_dense_inputs(bs, Q, P, cams, len(levels), G, dev)
+    out = torch.empty((bs, Q, C), device=dev)
+    esize = torch.finfo(dtype).bits // 8
+    table_bytes = feats.table.numel() * esize
+    fn = lambda: ops.deformable_aggregation(feats, None, None, loc, w, precision=precision, out=out)  # noqa: E731
+    med, best = time_fn(fn, reps, flush=table_bytes < 2 * L2)
+    tb = touched_bytes(feats, loc, esize)
+    alg = tb + loc.numel() * 4 + w.numel() * 4 + out.numel() * 4
+    gbs = alg / (med / 1e3) / 1e9
+    cams_total = bs * cams
+    return {"config": name, "path": "deformable_aggregation", "precision": precision, "dtype": str(dtype),
+            "cams": cams, "groups": G, "latency_us": med * 1e3, "best_us": best * 1e3,
+            "algorithmic_bytes": alg, "touched_feature_bytes": tb, "achieved_gbs": gbs, "frac": gbs / peak(),
+            "camera_frames_per_s": cams_total / (med / 1e3),
+            "streams_at_30fps_6layers": int(cams_total / (30 * 6 * med / 1e3)),
+            "l2": "flushed" if table_bytes < 2 * L2 else "table > L2"}
+
+
+def ring(cams, radius=12.0, height=4.0, focal=300.0, size=(704, 256)):
+    import numpy as np
+
+    Ks, Rs, ts = [], [], []
+    for i in range(cams):
+        ang = 2 * math.pi * i / cams
+        pos = np.array([radius * math.cos(ang), radius * math.sin(ang), height])
+        z = np.array([0.0, 0.0, 0.9]) - pos
+        z /= np.linalg.norm(z)
+        x = np.cross(z, [0.0, 0.0, 1.0])
+        x /= np.linalg.norm(x)
+        y = np.cross(z, x)
+        R = np.vstack([x, y, z])
+        Ks.append([focal, focal, size[0] / 2, size[1] / 2])
+        Rs.append(R)
+        ts.append(-R @ pos)
+    return np.array(Ks), np.array(Rs), np.array(ts)
+
+
+def anchors_for(Q, dev, seed=2):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    a = torch.zeros((Q, 10))
+    a[:, 0:2] = torch.rand((Q, 2), generator=g) * 8 - 4
+    a[:, 2] = 0.9
+    a[:, 3:6] = torch.tensor([0.6, 0.6, 1.8])
+    a[:, 6] = torch.rand(Q, generator=g) * 2 * math.pi - math.pi
+    return a.to(dev)
+
+
+def project_case(reps, dev, cams=6, C=256, G=8, Q=900):
+    feats = make_feats(cams, CFG1_LEVELS, C, torch.float32, dev)
+    K, R, T = ring(cams)
+    camd = ops.Cameras(K, R, T, device=dev)
+    anchors = anchors_for(Q, dev).unsqueeze(0)
+    offs = (torch.rand((6, 3), generator=torch.Generator().manual_seed(3)) * 2 - 1)
+    _, w = make_dense_inputs(1, Q, 13, cams, 4, G, dev)
+    out = torch.empty((1, Q, C), device=dev)
+    fn = lambda: ops.msda_dense_project(feats, anchors, offs, camd, [4.0, 8.0, 16.0, 32.0], w, dt=0.1,  # noqa
+                                        out=out)
+    med, best = time_fn(fn, reps, flush=True)
+    return {"config": "cfg1-project", "path": "msda_dense_project (fused keypoints + projection)",
+            "precision": "fast", "dtype": "float32", "cams": cams, "latency_us": med * 1e3, "best_us": best * 1e3,
+            "camera_frames_per_s": cams / (med / 1e3)}
+
+
+def oae_case(reps, dev, cams=32, C=256, Q=900):
+    feats = make_feats(cams, CFG1_LEVELS, C, torch.bfloat16, dev)
+    K, R, T = ring(cams)
+    camd = ops.Cameras(K, R, T, device=dev)
+    anchors = anchors_for(Q, dev)
+    offs = (torch.rand((6, 3), generator=torch.Generator().manual_seed(3)) * 2 - 1)
+    g = torch.Generator(device=dev).manual_seed(4)
+    desc = torch.randn((Q, C), generator=g, device=dev)
+    vis = torch.rand((Q, cams), generator=g, device=dev)
+    mem = torch.nn.functional.normalize(torch.randn((Q, C), generator=g, device=dev), dim=1)
+    fn = lambda: ops.oae_pool(feats, anchors, offs, camd, [4.0, 8.0, 16.0, 32.0], desc, vis, mem,  # noqa
+                              check=False)
+    med, best = time_fn(fn, reps, flush=False)
+    return {"config": "cfg4-oae", "path": "oae_pool (keypoint sampling + softmax + visibility fusion)",
+            "dtype": "bfloat16", "cams": cams, "latency_us": med * 1e3, "best_us": best * 1e3,
+            "queries_per_s": Q / (med / 1e3)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--only", default="")
+    args = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    cases = {
+        "cfg1d": lambda: dense_case("cfg1 Sparse4D default (6 cams, G=8)", 6, CFG1_LEVELS, 256, 8, torch.float32,
+                                    "fast", args.reps, dev),
+        "cfg1d_exact": lambda: dense_case("cfg1 Sparse4D default, exact", 6, CFG1_LEVELS, 256, 8, torch.float32,
+                                          "exact", max(3, args.reps // 4), dev),
+        "cfg2d": lambda: dense_case("cfg2 warehouse 16x1080p (dense, G=8)", 16, CFG2_LEVELS, 256, 8,
+                                    torch.float32, "fast", args.reps, dev),
+        "cfg3": lambda: dense_case("cfg3 64 cams fp16 (per decoder layer)", 64, CFG1_LEVELS, 256, 8,
+                                   torch.float16, "fast", args.reps, dev),
+        "cfg5": lambda: dense_case("cfg5 512 cams fp16 (1 GPU)", 512, CFG1_LEVELS, 256, 8, torch.float16, "fast",
+                                   max(5, args.reps // 4), dev),
+        "project": lambda: project_case(args.reps, dev),
+        "cfg4": lambda: oae_case(max(5, args.reps // 4), dev),
+    }
+    for name, fn in cases.items():
+        if args.only and name not in args.only.split(","):
+            continue
+        try:
+            print(json.dumps(fn()), flush=True)
+        except Exception as e:  # keep going: one line per case
+            print(json.dumps({"config": name, "error": repr(e)}), flush=True)
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
