@@ -213,6 +213,211 @@ __global__ void __launch_bounds__(kDenseThreads) dense_fast_kernel(DenseArgs a) 
   }
 }
 
+// ---------------------------------------------------------------------------
+// FAST, production shape (C == 32 * VEC): one CTA of kWcWarps warps per
+// anchor; warp w aggregates cameras w, w + kWcWarps, ... in camera-major,
+// level-minor order, so all resident anchors sweep the cameras in lockstep and
+// the live working set is a few cameras' maps (L2-resident): each touched cell
+// comes from HBM about once.  Per camera, lanes build 32 sample records and
+// stage the group weights in warp-private shared memory (__syncwarp only, no
+// CTA barrier), then the whole warp gathers each sample's four corner rows
+// (lane = VEC channels, 16/32-B vector loads, full sectors) and FMAs them with
+// iw_k * w_g: FFMA2 in f32, or HFMA2 into a per-camera half2 partial that is
+// flushed to f32 after every camera (HACC, f16 storage; the paper's half2
+// accumulation, bounded to 52-sample runs).
+
+constexpr int kWcWarps = 4;
+constexpr int kWcMaxGroups = 32;
+
+template <int NV>
+struct Row {
+  uint4 v[NV];
+};
+
+template <int NV>
+__device__ __forceinline__ Row<NV> ld_row(const char* p) {
+  Row<NV> r;
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.v[i].x), "=r"(r.v[i].y), "=r"(r.v[i].z), "=r"(r.v[i].w)
+                 : "l"(p + 16 * i));
+  return r;
+}
+
+// VEC stored elements (packed in 32-bit words) -> f32, exact
+template <typename T, int VEC>
+__device__ __forceinline__ void raw_to_f32(const uint32_t* raw, float* f) {
+  if constexpr (sizeof(T) == 4) {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) f[e] = __uint_as_float(raw[e]);
+  } else if constexpr (std::is_same<T, __half>::value) {
+#pragma unroll
+    for (int e = 0; e < VEC / 2; ++e) {
+      const float2 p = __half22float2(*reinterpret_cast<const __half2*>(&raw[e]));
+      f[2 * e] = p.x;
+      f[2 * e + 1] = p.y;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC / 2; ++e) {  // bf16 -> f32 is a 16-bit shift
+      f[2 * e] = __uint_as_float(raw[e] << 16);
+      f[2 * e + 1] = __uint_as_float(raw[e] & 0xffff0000u);
+    }
+  }
+}
+
+template <typename T, int VEC, bool PROJECT, bool HACC>
+__global__ void __launch_bounds__(kWcWarps * 32) dense_warpcam_kernel(DenseArgs a) {
+  constexpr int NV = VEC * (int)sizeof(T) / 16;
+  static_assert(NV >= 1 && NV * 16 == VEC * (int)sizeof(T), "16-B multiples");
+  __shared__ SampleRec s_rec[kWcWarps][32];
+  __shared__ float s_w[kWcWarps][32 * kWcMaxGroups];
+  __shared__ float s_red[kWcWarps][32 * VEC];
+  __shared__ float s_ws[kWcWarps][kWcMaxGroups];
+  __shared__ double s_kp[PROJECT ? kMaxPoints * 3 : 1];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t bq = blockIdx.x;
+  const int b = (int)(bq / a.Q);
+  const int G = a.G;
+  const int cpg = a.C / G;
+  const int c0 = lane * VEC;
+  const int g = c0 / cpg;
+  const bool group_head = (c0 % cpg) == 0;
+  const int64_t row_base = (int64_t)b * a.n_rows;
+  const char* feat = reinterpret_cast<const char*>(a.feat) + (size_t)c0 * sizeof(T);
+  const uint32_t row_bytes = (uint32_t)(a.C * (int)sizeof(T));
+  const int n_cs = a.P * a.L;  // samples per camera
+
+  if constexpr (PROJECT) {
+    anchor_keypoints(a, bq, s_kp, a.status);
+    __syncthreads();
+  }
+
+  float acc[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) acc[e] = 0.0f;
+  float wsum = 0.0f;
+
+  for (int cam = warp; cam < a.cams; cam += kWcWarps) {
+    __half2 hacc[VEC / 2];
+    if constexpr (HACC) {
+#pragma unroll
+      for (int e = 0; e < VEC / 2; ++e) hacc[e] = __float2half2_rn(0.0f);
+    }
+    for (int base = 0; base < n_cs; base += 32) {
+      const int n = min(32, n_cs - base);
+      if (lane < n) {
+        const int s = base + lane;
+        const int l = s / a.P, p = s - l * a.P;
+        const int t = cam * a.L + l;
+        const int H = a.shape[2 * t], W = a.shape[2 * t + 1];
+        float u, v;
+        bool valid = true;
+        if constexpr (PROJECT) {
+          double up, vp;
+          valid = project_point(a, cam, s_kp + 3 * p, up, vp);
+          const double st = (double)a.strides[l];
+          u = valid ? (float)(up / st - 0.5) : -4.0f;
+          v = valid ? (float)(vp / st - 0.5) : -4.0f;
+        } else {
+          const float* lp = a.loc + ((bq * a.P + p) * a.cams + cam) * 2;
+          u = __fsub_rn(__fmul_rn(lp[0], (float)W), 0.5f);
+          v = __fsub_rn(__fmul_rn(lp[1], (float)H), 0.5f);
+        }
+        s_rec[warp][lane] = make_record(u, v, row_base + a.start[t], H, W);
+        const float* wp = a.w + (((bq * a.P + p) * a.cams + cam) * a.L + l) * (int64_t)G;
+        for (int gg = 0; gg < G; ++gg) s_w[warp][lane * G + gg] = valid ? __ldg(wp + gg) : 0.0f;
+      }
+      __syncwarp();
+      for (int i = 0; i < n; i += 2) {
+        const bool two = i + 1 < n;
+        const SampleRec r0 = s_rec[warp][i];
+        const SampleRec r1 = s_rec[warp][two ? i + 1 : i];
+        const float w0 = s_w[warp][i * G + g];
+        const float w1 = two ? s_w[warp][(i + 1) * G + g] : 0.0f;
+        Row<NV> c[2][4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (r0.row[k] >= 0) c[0][k] = ld_row<NV>(feat + (size_t)r0.row[k] * row_bytes);
+          else
+#pragma unroll
+            for (int j = 0; j < NV; ++j) c[0][k].v[j] = make_uint4(0, 0, 0, 0);
+          if (two && r1.row[k] >= 0) c[1][k] = ld_row<NV>(feat + (size_t)r1.row[k] * row_bytes);
+          else
+#pragma unroll
+            for (int j = 0; j < NV; ++j) c[1][k].v[j] = make_uint4(0, 0, 0, 0);
+        }
+        wsum += w0 + w1;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const SampleRec& r = j ? r1 : r0;
+          const float wg = j ? w1 : w0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float cw = r.iw[k] * wg;
+            const uint32_t* raw = reinterpret_cast<const uint32_t*>(c[j][k].v);
+            if constexpr (HACC) {
+              const __half2 cwh = __float2half2_rn(cw);
+#pragma unroll
+              for (int e = 0; e < VEC / 2; ++e)
+                hacc[e] = __hfma2(*reinterpret_cast<const __half2*>(&raw[e]), cwh, hacc[e]);
+            } else {
+              float f[VEC];
+              raw_to_f32<T, VEC>(raw, f);
+#pragma unroll
+              for (int e = 0; e < VEC; e += 2) {
+                const float2 pr = __ffma2_rn(make_float2(f[e], f[e + 1]), make_float2(cw, cw),
+                                             make_float2(acc[e], acc[e + 1]));
+                acc[e] = pr.x;
+                acc[e + 1] = pr.y;
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+    if constexpr (HACC) {
+#pragma unroll
+      for (int e = 0; e < VEC / 2; ++e) {
+        const float2 f = __half22float2(hacc[e]);
+        acc[2 * e] += f.x;
+        acc[2 * e + 1] += f.y;
+      }
+    }
+  }
+
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) s_red[warp][c0 + e] = acc[e];
+  if (group_head) s_ws[warp][g] = wsum;
+  __syncthreads();
+  float* o = a.out + bq * a.C;
+  for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
+    float sum = 0.0f;
+#pragma unroll
+    for (int j = 0; j < kWcWarps; ++j) sum += s_red[j][c];
+    if (a.normalize) {
+      const int gg = c / cpg;
+      float ws = 0.0f;
+#pragma unroll
+      for (int j = 0; j < kWcWarps; ++j) ws += s_ws[j][gg];
+      if (ws == 0.0f) set_status(a.status, MSDA_ZERO_WEIGHT_SUM, bq);
+      sum = sum / ws;
+    }
+    o[c] = sum;
+  }
+}
+
+template <typename T, int VEC, bool PROJECT, bool HACC>
+cudaError_t launch_warpcam(const DenseArgs& a, cudaStream_t s) {
+  const int64_t grid = (int64_t)a.bs * a.Q;
+  if (grid == 0) return cudaSuccess;
+  dense_warpcam_kernel<T, VEC, PROJECT, HACC><<<(unsigned)grid, kWcWarps * 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <typename T, int VEC, bool PROJECT>
 cudaError_t launch_dense_fast_t(const DenseArgs& a, cudaStream_t s) {
   const int64_t grid = (int64_t)a.bs * a.Q;
@@ -225,6 +430,22 @@ template <bool PROJECT>
 cudaError_t launch_dense_fast(const DenseArgs& a, int dtype, cudaStream_t s) {
   const int cpg = a.C / a.G;
   const auto fits = [&](int vec) { return a.C % vec == 0 && cpg % vec == 0 && a.C / vec <= kDenseThreads; };
+  const uintptr_t al = reinterpret_cast<uintptr_t>(a.feat);
+  const auto warpcam = [&](int vec, int esz) {
+    return a.C == 32 * vec && cpg % vec == 0 && a.G <= kWcMaxGroups && al % 16 == 0 && (a.C * esz) % 16 == 0;
+  };
+  switch (dtype) {
+    case MSDA_F32:
+      if (warpcam(8, 4)) return launch_warpcam<float, 8, PROJECT, false>(a, s);
+      if (warpcam(4, 4)) return launch_warpcam<float, 4, PROJECT, false>(a, s);
+      break;
+    case MSDA_F16:
+      if (warpcam(8, 2)) return launch_warpcam<__half, 8, PROJECT, true>(a, s);
+      break;
+    default:
+      if (warpcam(8, 2)) return launch_warpcam<__nv_bfloat16, 8, PROJECT, false>(a, s);
+      break;
+  }
   switch (dtype) {
     case MSDA_F32:
       if (fits(4)) return launch_dense_fast_t<float, 4, PROJECT>(a, s);
@@ -257,14 +478,17 @@ __global__ void dense_expand_kernel(DenseArgs a, int group, int64_t* offsets, in
     offsets[bq] = bq * S;
     if (bq == (int64_t)a.bs * a.Q - 1) offsets[bq + 1] = (bq + 1) * S;
   }
+  // emitted camera-major, level, point: already grouped by (camera, level),
+  // so the canonicaliser takes its rank-within-run path
   for (int s = threadIdx.x; s < S; s += blockDim.x) {
-    const int l = s % a.L;
-    const int pc = s / a.L;
-    const int cam = pc % a.cams;
-    const int p = pc / a.cams;
+    const int p = s % a.P;
+    const int cl = s / a.P;
+    const int l = cl % a.L;
+    const int cam = cl / a.L;
     const int t = cam * a.L + l;
     const int64_t o = bq * S + s;
-    float u, v, w = a.w[o * a.G + group];
+    const int64_t wi = ((bq * a.P + p) * a.cams + cam) * a.L + l;
+    float u, v, w = a.w[wi * a.G + group];
     if constexpr (PROJECT) {
       double up, vp;
       if (project_point(a, cam, s_kp + 3 * p, up, vp)) {
