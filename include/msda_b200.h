@@ -63,8 +63,11 @@ enum msda_dtype { MSDA_F32 = 0, MSDA_F16 = 1, MSDA_BF16 = 2 };
  *  MSDA_EXACT_HALF f16 storage and f16 arithmetic/accumulation, bit-identical
  *                  to msda_optimized(PACKED_HALF) (features.py:306-416).
  *  MSDA_FAST       FMA arithmetic, any summation order, f32 accumulation;
- *                  tolerance parity (1e-4 rel. fp32, 1e-2 fp16/bf16).          */
-enum msda_precision { MSDA_EXACT = 0, MSDA_EXACT_HALF = 1, MSDA_FAST = 2 };
+ *                  tolerance parity (1e-4 rel. fp32, 1e-2 fp16/bf16).
+ *  MSDA_FAST_H2    dense path, f16 storage: products and per-camera partial
+ *                  sums in half2 (the paper's half2 accumulation), flushed to
+ *                  f32 per camera; 1e-2 tolerance.  Other dtypes: = FAST.      */
+enum msda_precision { MSDA_EXACT = 0, MSDA_EXACT_HALF = 1, MSDA_FAST = 2, MSDA_FAST_H2 = 3 };
 
 /* Multi-camera multi-level feature table: channel-last rows, every
  * (camera, level) grid (H, W, C) row-major, concatenated camera-major then

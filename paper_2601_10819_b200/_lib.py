@@ -25,7 +25,7 @@ MSDA_BAD_ARG = 8
 MSDA_OFFSET_RANGE = 9
 
 MSDA_F32, MSDA_F16, MSDA_BF16 = 0, 1, 2
-MSDA_EXACT, MSDA_EXACT_HALF, MSDA_FAST = 0, 1, 2
+MSDA_EXACT, MSDA_EXACT_HALF, MSDA_FAST, MSDA_FAST_H2 = 0, 1, 2, 3
 
 P = ctypes.c_void_p
 I32 = ctypes.c_int32

@@ -87,7 +87,7 @@ int32_t msda_csr_stages(const msda_features_t* feat, const msda_csr_plan_t* plan
   int32_t st = validate_features(feat);
   if (st != MSDA_OK) return st;
   if (!plan || plan->n_queries < 0 || plan->n_samples < 0) return MSDA_BAD_ARG;
-  if (precision != MSDA_EXACT && precision != MSDA_EXACT_HALF && precision != MSDA_FAST) return MSDA_BAD_PRECISION;
+  if (precision < MSDA_EXACT || precision > MSDA_FAST_H2) return MSDA_BAD_PRECISION;
   if (precision == MSDA_EXACT_HALF && feat->dtype != MSDA_F16) return MSDA_BAD_ARG;
   if (!workspace || workspace_bytes < msda_csr_workspace_size(plan->n_queries, plan->n_samples, feat->channels))
     return MSDA_BAD_ARG;
@@ -97,12 +97,11 @@ int32_t msda_csr_stages(const msda_features_t* feat, const msda_csr_plan_t* plan
     return MSDA_BAD_ARG;
   cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
   ExactWorkspace w = carve_exact_workspace(workspace, plan->n_samples);
-  if ((stage_mask & 1) && cudaMemsetAsync(w.status, 0, sizeof(DevStatus), stream) != cudaSuccess)
-    return MSDA_CUDA_ERROR;
+  if ((stage_mask & 1) && reset_exact_workspace(w, stream) != cudaSuccess) return MSDA_CUDA_ERROR;
   if (plan->n_queries == 0) return MSDA_OK;
   // FAST on the CSR path runs the exact kernels: they already sit on the
   // gather roofline for the reference plan shapes.
-  const int prec = precision == MSDA_FAST ? MSDA_EXACT : precision;
+  const int prec = precision >= MSDA_FAST ? MSDA_EXACT : precision;
   if ((stage_mask & 1) &&
       launch_plan_canon(*feat, *plan, normalize, w, num_sms_for_current_device(), stream) != cudaSuccess)
     return MSDA_CUDA_ERROR;

@@ -427,7 +427,7 @@ cudaError_t launch_dense_fast_t(const DenseArgs& a, cudaStream_t s) {
 }
 
 template <bool PROJECT>
-cudaError_t launch_dense_fast(const DenseArgs& a, int dtype, cudaStream_t s) {
+cudaError_t launch_dense_fast(const DenseArgs& a, int dtype, bool h2, cudaStream_t s) {
   const int cpg = a.C / a.G;
   const auto fits = [&](int vec) { return a.C % vec == 0 && cpg % vec == 0 && a.C / vec <= kDenseThreads; };
   const uintptr_t al = reinterpret_cast<uintptr_t>(a.feat);
@@ -440,7 +440,8 @@ cudaError_t launch_dense_fast(const DenseArgs& a, int dtype, cudaStream_t s) {
       if (warpcam(4, 4)) return launch_warpcam<float, 4, PROJECT, false>(a, s);
       break;
     case MSDA_F16:
-      if (warpcam(8, 2)) return launch_warpcam<__half, 8, PROJECT, true>(a, s);
+      if (warpcam(8, 2) && h2) return launch_warpcam<__half, 8, PROJECT, true>(a, s);
+      if (warpcam(8, 2)) return launch_warpcam<__half, 8, PROJECT, false>(a, s);
       break;
     default:
       if (warpcam(8, 2)) return launch_warpcam<__nv_bfloat16, 8, PROJECT, false>(a, s);
@@ -587,10 +588,12 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
   if (ws_bytes < exact_workspace_bytes(nq, S) + dense_exact_extra_bytes(nq, S)) return MSDA_BAD_ARG;
   ExactWorkspace ew = carve_exact_workspace(ws, S);
   a.status = ew.status;
-  if (cudaMemsetAsync(ew.status, 0, sizeof(DevStatus), s) != cudaSuccess) return MSDA_CUDA_ERROR;
+  if (reset_exact_workspace(ew, s) != cudaSuccess) return MSDA_CUDA_ERROR;
   if (nq == 0) return MSDA_OK;
-  if (precision == MSDA_FAST) {
-    const cudaError_t e = project ? launch_dense_fast<true>(a, f->dtype, s) : launch_dense_fast<false>(a, f->dtype, s);
+  if (precision == MSDA_FAST || precision == MSDA_FAST_H2) {
+    const bool h2 = precision == MSDA_FAST_H2;
+    const cudaError_t e =
+        project ? launch_dense_fast<true>(a, f->dtype, h2, s) : launch_dense_fast<false>(a, f->dtype, h2, s);
     return e == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
   }
   if (precision == MSDA_EXACT_HALF && f->dtype != MSDA_F16) return MSDA_BAD_ARG;
@@ -639,7 +642,7 @@ int32_t msda_dense(const msda_features_t* feat, int32_t n_queries, int32_t n_poi
                    float* out, void* workspace, size_t workspace_bytes, void* stream) {
   int32_t st = validate_dense(feat, n_queries, n_points, n_groups);
   if (st != MSDA_OK) return st;
-  if (precision < MSDA_EXACT || precision > MSDA_FAST) return MSDA_BAD_PRECISION;
+  if (precision < MSDA_EXACT || precision > MSDA_FAST_H2) return MSDA_BAD_PRECISION;
   if (!sampling_location || !weights || !out || !workspace) return MSDA_BAD_ARG;
   return run_dense(feat, n_queries, n_points, n_groups, sampling_location, weights, precision, normalize, out,
                    workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream), false, nullptr, 0, nullptr,
@@ -653,7 +656,7 @@ int32_t msda_dense_project(const msda_features_t* feat, int32_t n_queries, const
   const int32_t P = 7 + n_learned;
   int32_t st = validate_dense(feat, n_queries, P, n_groups);
   if (st != MSDA_OK) return st;
-  if (precision < MSDA_EXACT || precision > MSDA_FAST) return MSDA_BAD_PRECISION;
+  if (precision < MSDA_EXACT || precision > MSDA_FAST_H2) return MSDA_BAD_PRECISION;
   if (n_learned < 0 || P > kMaxPoints || (n_learned > 0 && !learned_offsets)) return MSDA_BAD_ARG;
   if (!anchors || !cams || !cams->K || !cams->R || !cams->t || !strides || !weights || !out || !workspace)
     return MSDA_BAD_ARG;

@@ -4,8 +4,11 @@
 
 namespace msda {
 
+constexpr size_t kZeroRowBytes = 8192;  // a row of zeros for out-of-grid corners (C * esize <= 8 KB)
+
 struct ExactWorkspace {
   DevStatus* status;
+  void* zero_row;
   SampleRec* rec;
   float* wn;
   unsigned long long* g_hi;
@@ -14,6 +17,7 @@ struct ExactWorkspace {
 };
 
 size_t exact_workspace_bytes(int64_t n_queries, int64_t n_samples);
+cudaError_t reset_exact_workspace(const ExactWorkspace& w, cudaStream_t stream);
 ExactWorkspace carve_exact_workspace(void* ws, int64_t n_samples);
 cudaError_t launch_plan_canon(const msda_features_t& f, const msda_csr_plan_t& p, int normalize,
                               const ExactWorkspace& w, int num_sms, cudaStream_t stream,

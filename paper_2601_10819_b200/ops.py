@@ -25,7 +25,7 @@ from . import _lib as L
 from .errors import raise_for_status
 
 _DTYPES = {torch.float32: L.MSDA_F32, torch.float16: L.MSDA_F16, torch.bfloat16: L.MSDA_BF16}
-_PREC = {"exact": L.MSDA_EXACT, "exact_half": L.MSDA_EXACT_HALF, "fast": L.MSDA_FAST}
+_PREC = {"exact": L.MSDA_EXACT, "exact_half": L.MSDA_EXACT_HALF, "fast": L.MSDA_FAST, "fast_h2": L.MSDA_FAST_H2}
 
 
 def _ptr(t):

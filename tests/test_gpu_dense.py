@@ -97,6 +97,9 @@ def test_dense_fast_half_storage(cuda_dev, dt):
     assert rel(out, ref_r) <= 1e-4  # only summation order / FMA differ from the pre-rounded reference
     ex = ops.deformable_aggregation(feats, None, None, t(loc), t(wts), precision="exact", check=True).cpu().numpy()
     assert ex.tobytes() == ref_r.tobytes()
+    # the paper's half2 accumulation (f16 products and per-camera partials): north_star fp16 bound only
+    h2 = ops.deformable_aggregation(feats, None, None, t(loc), t(wts), precision="fast_h2", check=True).cpu().numpy()
+    assert np.abs(h2 - ref).max() / max(1.0, np.abs(ref).max()) <= 1e-2
 
 
 def _ring(n, radius=12.0, height=4.0, focal=300.0, size=(704, 256)):

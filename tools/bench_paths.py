@@ -195,6 +195,8 @@ def main():
                                     torch.float32, "fast", args.reps, dev),
         "cfg3": lambda: dense_case("cfg3 64 cams fp16 (per decoder layer)", 64, CFG1_LEVELS, 256, 8,
                                    torch.float16, "fast", args.reps, dev),
+        "cfg3_h2": lambda: dense_case("cfg3 64 cams fp16, half2 accumulation", 64, CFG1_LEVELS, 256, 8,
+                                      torch.float16, "fast_h2", args.reps, dev),
         "cfg5": lambda: dense_case("cfg5 512 cams fp16 (1 GPU)", 512, CFG1_LEVELS, 256, 8, torch.float16, "fast",
                                    max(5, args.reps // 4), dev),
         "project": lambda: project_case(args.reps, dev),
