@@ -33,6 +33,7 @@
 //   gather_exact_kernel register-pipelined fallback for channel slices that do
 //                       not span whole warps (small C in tests / odd groups).
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "msda_common.cuh"
@@ -115,15 +116,20 @@ __device__ __forceinline__ float key_weight(u64 lo) { return unord_f32((uint32_t
 // Canonicalise one query whose n keys sit in (khi, klo).  On return
 // sdst[i] = canonical slot of key i and sw[slot] = its weight; keys are
 // either untouched (rank path) or sorted in place with sdst[i] = i.
-__device__ void canon_slots(int n, u64* khi, u64* klo, int32_t* sdst, float* sw) {
+constexpr int kRunTable = 2048;  // tiles whose run start is tabulated in shared memory
+
+__device__ void canon_slots(int n, int n_tiles, u64* khi, u64* klo, int32_t* sdst, float* sw, int16_t* s_run) {
   bool bad = false;
   for (int i = threadIdx.x + 1; i < n; i += blockDim.x) bad |= (khi[i] >> 32) < (khi[i - 1] >> 32);
   bool rank_path = !__syncthreads_or(bad);
+  const bool table = n_tiles <= kRunTable && n <= 32767;
   if (rank_path) {
     bool long_run = false;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       if (i > 0 && (khi[i] >> 32) == (khi[i - 1] >> 32)) continue;  // run heads probe their run
-      long_run |= (tile_lower_bound(khi, n, (uint32_t)(khi[i] >> 32) + 1) - i) > kRunCap;
+      const uint32_t t = (uint32_t)(khi[i] >> 32);
+      if (table) s_run[t] = (int16_t)i;
+      long_run |= (tile_lower_bound(khi, n, t + 1) - i) > kRunCap;
     }
     rank_path = !__syncthreads_or(long_run);
   }
@@ -131,13 +137,22 @@ __device__ void canon_slots(int n, u64* khi, u64* klo, int32_t* sdst, float* sw)
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const u64 ih = khi[i], il = klo[i];
       const uint32_t t = (uint32_t)(ih >> 32);
-      const int rs = tile_lower_bound(khi, n, t);
+      const int rs = table ? (int)s_run[t] : tile_lower_bound(khi, n, t);
+      // inside a run the order is (v, u) as one 64-bit key, then weight, then position
+      const u64 pi = (ih << 32) | (il >> 32);
+      const uint32_t wi = (uint32_t)il;
       int rank = 0;
       for (int j = rs; j < n; ++j) {
         const u64 jh = khi[j];
         if ((uint32_t)(jh >> 32) != t) break;
         const u64 jl = klo[j];
-        rank += (jh < ih || (jh == ih && (jl < il || (jl == il && j < i)))) ? 1 : 0;
+        const u64 pj = (jh << 32) | (jl >> 32);
+        if (pj < pi) {
+          ++rank;
+        } else if (pj == pi) {
+          const uint32_t wj = (uint32_t)jl;
+          rank += (wj < wi || (wj == wi && j < i)) ? 1 : 0;
+        }
       }
       sdst[i] = rs + rank;
       sw[rs + rank] = key_weight(il);
@@ -180,6 +195,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_canon_kernel(PlanArgs a) {
   __shared__ __align__(16) u64 s_lo[kPlanSmemCap];
   __shared__ __align__(16) float s_w[kPlanSmemCap];
   __shared__ __align__(16) int32_t s_dst[kPlanSmemCap];
+  __shared__ int16_t s_run[kRunTable];
   __shared__ float s_wsum;
   const int n_tiles = a.n_cams * a.n_levels;
 
@@ -206,7 +222,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_canon_kernel(PlanArgs a) {
       klo[i] = ((u64)ord_f32(uu) << 32) | ord_f32(ww);
     }
     __syncthreads();
-    canon_slots(n, khi, klo, sdst, sw);
+    canon_slots(n, n_tiles, khi, klo, sdst, sw, s_run);
     if (threadIdx.x == 0) {
       float ws = 0.0f;
       if (a.normalize) {
@@ -557,213 +573,6 @@ cudaError_t launch_gather_pipe(const GatherArgs& g, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------------------
-// Bulk-copy gather: one warp owns a whole query row (C == 32 * VEC channels).
-// Per sample, one elected lane issues four cp.async.bulk copies (the TMA bulk
-// engine; SASS UBLKCP) of complete corner rows — out-of-grid corners copy a
-// zero row kept in the workspace — into a D-deep shared-memory ring whose
-// slots complete on an mbarrier (expect_tx bytes).  Every lane then reads its
-// VEC channels of the four rows and runs the exact FFMA2 tree.  Per sample
-// that is ~4 bulk requests + 4-8 LDS + 2*VEC FFMA2 per warp instead of 32
-// lane-level LDGSTS per corner per 128 channels.
-
-struct BulkArgs {
-  GatherArgs g;
-  const void* zero_row;  // global row of zeros (C * esize bytes, 16-B aligned)
-};
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
-}
-
-template <int ROW, int D>
-struct BulkSmem {
-  static constexpr int kSlot = 4 * ROW;
-  static constexpr int kRing = D * kSlot;
-  static constexpr int kRows = 2 * 32 * 16;
-  static constexpr int kIw = 2 * 32 * 16;
-  static constexpr int kWn = 2 * 32 * 4;
-  static constexpr int kBar = D * 8;
-  static constexpr int kTotal = kRing + kRows + kIw + kWn + kBar;
-};
-
-template <typename T, int VEC, bool HALF, int D>
-__global__ void __launch_bounds__(32) gather_bulk_kernel(BulkArgs ba) {
-  const GatherArgs& a = ba.g;
-  constexpr int ROW = 32 * VEC * (int)sizeof(T);  // bytes per feature row (whole C)
-  constexpr int LB = VEC * (int)sizeof(T);        // bytes per lane per row
-  using SM = BulkSmem<ROW, D>;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int lane = threadIdx.x;
-  int4* s_rows = reinterpret_cast<int4*>(smem_raw + SM::kRing);
-  float4* s_iw = reinterpret_cast<float4*>(smem_raw + SM::kRing + SM::kRows);
-  float* s_wn = reinterpret_cast<float*>(smem_raw + SM::kRing + SM::kRows + SM::kIw);
-  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem_raw);
-  const uint32_t bars = ring + SM::kRing + SM::kRows + SM::kIw + SM::kWn;
-
-  const int64_t q = blockIdx.x;
-  if (q >= a.n_queries) return;
-  const int64_t lo = a.offsets[q];
-  const int n = (int)(a.offsets[q + 1] - lo);
-  const SampleRec* rec = a.rec + lo;
-  const float* wnp = a.wn + lo;
-  const char* feat = reinterpret_cast<const char*>(a.feat);
-  const char* zrow = reinterpret_cast<const char*>(ba.zero_row);
-
-  if (lane == 0)
-    for (int s = 0; s < D; ++s) mbar_init(bars + 8 * s, 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncwarp();
-
-  int4 r_rows = make_int4(-1, -1, -1, -1);
-  float4 r_iw = make_float4(0.f, 0.f, 0.f, 0.f);
-  float r_wn = 0.0f;
-  auto load_batch = [&](int b) {
-    const int s = b * 32 + lane;
-    if (s < n) {
-      const SampleRec r = ld_rec(rec + s);
-      r_rows = make_int4(r.row[0], r.row[1], r.row[2], r.row[3]);
-      r_iw = make_float4(r.iw[0], r.iw[1], r.iw[2], r.iw[3]);
-      r_wn = __ldg(wnp + s);
-    }
-  };
-  auto store_batch = [&](int buf) {
-    s_rows[buf * 32 + lane] = r_rows;
-    s_iw[buf * 32 + lane] = r_iw;
-    s_wn[buf * 32 + lane] = r_wn;
-  };
-  auto src_of = [&](int row) -> const char* { return row >= 0 ? feat + (size_t)row * ROW : zrow; };
-  auto issue = [&](int k, int slot) {  // lane 0 only
-    const int4 rows = s_rows[((k >> 5) & 1) * 32 + (k & 31)];
-    const uint32_t bar = bars + 8 * slot;
-    const uint32_t dst = ring + slot * SM::kSlot;
-    mbar_expect_tx(bar, 4 * ROW);
-    bulk_g2s(dst, src_of(rows.x), ROW, bar);
-    bulk_g2s(dst + ROW, src_of(rows.y), ROW, bar);
-    bulk_g2s(dst + 2 * ROW, src_of(rows.z), ROW, bar);
-    bulk_g2s(dst + 3 * ROW, src_of(rows.w), ROW, bar);
-  };
-
-  load_batch(0);
-  store_batch(0);
-  __syncwarp();
-  load_batch(1);
-  if (lane == 0)
-    for (int k = 0; k < D && k < n; ++k) issue(k, k);
-
-  float accf[VEC];
-  __half2 acch[VEC / 2];
-#pragma unroll
-  for (int e = 0; e < VEC; ++e) accf[e] = 0.0f;
-#pragma unroll
-  for (int e = 0; e < VEC / 2; ++e) acch[e] = __float2half2_rn(0.0f);
-
-  int slot = 0;
-  uint32_t phase = 0;
-  for (int i = 0; i < n; ++i) {
-    mbar_wait(bars + 8 * slot, phase);
-    const int bi = ((i >> 5) & 1) * 32 + (i & 31);
-    const float4 iw = s_iw[bi];
-    const float wn = s_wn[bi];
-    const unsigned char* src = smem_raw + slot * SM::kSlot + lane * LB;
-    uint32_t raw[4][LB / 4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-      for (int j = 0; j < LB / 16; ++j)
-        *reinterpret_cast<uint4*>(&raw[k][4 * j]) = *reinterpret_cast<const uint4*>(src + k * ROW + 16 * j);
-    if constexpr (!HALF) {
-      float c[4][VEC];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if constexpr (sizeof(T) == 4) {
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) c[k][e] = __uint_as_float(raw[k][e]);
-        } else if constexpr (std::is_same<T, __half>::value) {
-#pragma unroll
-          for (int e = 0; e < VEC / 2; ++e) {
-            const float2 p = __half22float2(*reinterpret_cast<const __half2*>(&raw[k][e]));
-            c[k][2 * e] = p.x;
-            c[k][2 * e + 1] = p.y;
-          }
-        } else {
-#pragma unroll
-          for (int e = 0; e < VEC / 2; ++e) {
-            c[k][2 * e] = __uint_as_float(raw[k][e] << 16);
-            c[k][2 * e + 1] = __uint_as_float(raw[k][e] & 0xffff0000u);
-          }
-        }
-      }
-      exact_accumulate<VEC>(accf, c, iw, wn, a.one2, a.nz2);
-    } else {
-      const void* cvp[4] = {raw[0], raw[1], raw[2], raw[3]};
-      half_accumulate<VEC>(acch, cvp, iw, wn);
-    }
-    __syncwarp();  // every lane has read the slot before it is refilled
-    const int k = i + D;
-    if (k < n) {
-      if ((k & 31) == 0) {  // entering record batch k/32: publish it, prefetch the next
-        store_batch((k >> 5) & 1);
-        __syncwarp();
-        load_batch((k >> 5) + 1);
-      }
-      if (lane == 0) issue(k, slot);
-    }
-    if (++slot == D) {
-      slot = 0;
-      phase ^= 1u;
-    }
-  }
-
-  float* o = a.out + q * a.out_stride + lane * VEC;
-  if constexpr (!HALF) {
-#pragma unroll
-    for (int e = 0; e < VEC; e += 4)
-      *reinterpret_cast<float4*>(o + e) = make_float4(accf[e], accf[e + 1], accf[e + 2], accf[e + 3]);
-  } else {
-#pragma unroll
-    for (int e = 0; e < VEC / 2; ++e) {
-      const float2 f = __half22float2(acch[e]);
-      o[2 * e] = f.x;
-      o[2 * e + 1] = f.y;
-    }
-  }
-  if (lane == 0 && a.empty) a.empty[q] = (n == 0) ? 1 : 0;
-}
-
-template <typename T, int VEC, bool HALF, int D>
-cudaError_t launch_gather_bulk(const BulkArgs& b, cudaStream_t stream) {
-  constexpr int ROW = 32 * VEC * (int)sizeof(T);
-  const int smem = BulkSmem<ROW, D>::kTotal;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gather_bulk_kernel<T, VEC, HALF, D>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  if (b.g.n_queries == 0) return cudaSuccess;
-  gather_bulk_kernel<T, VEC, HALF, D><<<(unsigned)b.g.n_queries, 32, smem, stream>>>(b);
-  return cudaGetLastError();
-}
-
 template <typename T, int VEC, bool HALF>
 cudaError_t launch_gather(const GatherArgs& g, cudaStream_t stream) {
   if ((g.C / VEC) % 32 == 0 && g.C % VEC == 0) {
@@ -779,16 +588,23 @@ cudaError_t launch_gather(const GatherArgs& g, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+int f32_lane_bytes() {
+  static const int v = [] {
+    const char* e = getenv("MSDA_F32_LANE_BYTES");
+    return (e && atoi(e) == 8) ? 8 : 16;
+  }();
+  return v;
+}
+
 }  // namespace
 
 cudaError_t reset_exact_workspace(const ExactWorkspace& w, cudaStream_t stream) {
-  // status word + zero row are contiguous
-  return cudaMemsetAsync(w.status, 0, kStatusBytes + kZeroRowBytes, stream);
+  return cudaMemsetAsync(w.status, 0, sizeof(DevStatus), stream);
 }
 
 size_t exact_workspace_bytes(int64_t n_queries, int64_t n_samples) {
   (void)n_queries;
-  size_t b = kStatusBytes + kZeroRowBytes;
+  size_t b = kStatusBytes;
   b += align_up((size_t)n_samples * sizeof(SampleRec), 256);
   b += align_up((size_t)n_samples * sizeof(float), 256);
   b += 2 * align_up((size_t)n_samples * sizeof(u64), 256);
@@ -801,8 +617,6 @@ ExactWorkspace carve_exact_workspace(void* ws, int64_t n_samples) {
   char* p = reinterpret_cast<char*>(ws);
   w.status = reinterpret_cast<DevStatus*>(p);
   p += kStatusBytes;
-  w.zero_row = p;
-  p += kZeroRowBytes;
   w.rec = reinterpret_cast<SampleRec*>(p);
   p += align_up((size_t)n_samples * sizeof(SampleRec), 256);
   w.wn = reinterpret_cast<float*>(p);
@@ -872,24 +686,6 @@ cudaError_t launch_gather_exact(const msda_features_t& f, const msda_csr_plan_t&
   const uintptr_t base = reinterpret_cast<uintptr_t>(f.data) | ((size_t)c_off * esz) | ((size_t)f.channels * esz);
   const uintptr_t obase = reinterpret_cast<uintptr_t>(out) | ((size_t)c_off * 4) | ((size_t)f.channels * 4);
   const int C = c_count;
-  // whole rows, one warp per query: TMA bulk-copy ring
-  if (c_off == 0 && C == f.channels && reinterpret_cast<uintptr_t>(f.data) % 16 == 0 && obase % 16 == 0 &&
-      (size_t)C * esz <= kZeroRowBytes) {
-    BulkArgs b{g, w.zero_row};
-    if (precision == MSDA_EXACT_HALF) {
-      if (C == 256) return launch_gather_bulk<__half, 8, true, 8>(b, stream);
-      if (C == 128) return launch_gather_bulk<__half, 4, true, 8>(b, stream);
-    } else if (f.dtype == MSDA_F32) {
-      if (C == 256) return launch_gather_bulk<float, 8, false, 6>(b, stream);
-      if (C == 128) return launch_gather_bulk<float, 4, false, 8>(b, stream);
-    } else if (f.dtype == MSDA_F16) {
-      if (C == 256) return launch_gather_bulk<__half, 8, false, 8>(b, stream);
-      if (C == 128) return launch_gather_bulk<__half, 4, false, 8>(b, stream);
-    } else {
-      if (C == 256) return launch_gather_bulk<__nv_bfloat16, 8, false, 8>(b, stream);
-      if (C == 128) return launch_gather_bulk<__nv_bfloat16, 4, false, 8>(b, stream);
-    }
-  }
   if (precision == MSDA_EXACT_HALF) {
     if (C % 128 == 0 && base % 8 == 0) return launch_gather<__half, 4, true>(g, stream);
     if (C % 8 == 0 && base % 16 == 0) return launch_gather<__half, 8, true>(g, stream);
@@ -898,6 +694,8 @@ cudaError_t launch_gather_exact(const msda_features_t& f, const msda_csr_plan_t&
   }
   switch (f.dtype) {
     case MSDA_F32:
+      // two warps per 256 channels (16-B lanes) or, with MSDA_F32_LANE_BYTES=8, four (8-B lanes)
+      if (f32_lane_bytes() == 8 && C % 64 == 0 && base % 8 == 0) return launch_gather<float, 2, false>(g, stream);
       if (C % 4 == 0 && base % 16 == 0 && obase % 16 == 0) return launch_gather<float, 4, false>(g, stream);
       return launch_gather<float, 2, false>(g, stream);
     case MSDA_F16:

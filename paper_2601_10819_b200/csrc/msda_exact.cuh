@@ -4,11 +4,8 @@
 
 namespace msda {
 
-constexpr size_t kZeroRowBytes = 8192;  // a row of zeros for out-of-grid corners (C * esize <= 8 KB)
-
 struct ExactWorkspace {
   DevStatus* status;
-  void* zero_row;
   SampleRec* rec;
   float* wn;
   unsigned long long* g_hi;
