@@ -190,6 +190,10 @@ __device__ __forceinline__ float sequential_sum(const float* sw, int n, bool vec
   return ws;
 }
 
+template <bool SMEM>
+__device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_t lo, int n, int n_tiles, u64* khi,
+                                            u64* klo, float* sw, int32_t* sdst, int16_t* s_run, float* s_wsum);
+
 __global__ void __launch_bounds__(kPlanThreads) plan_canon_kernel(PlanArgs a) {
   __shared__ __align__(16) u64 s_hi[kPlanSmemCap];
   __shared__ __align__(16) u64 s_lo[kPlanSmemCap];
@@ -203,11 +207,19 @@ __global__ void __launch_bounds__(kPlanThreads) plan_canon_kernel(PlanArgs a) {
     const int64_t lo = a.offsets[q], hi = a.offsets[q + 1];
     const int n = (int)(hi - lo);
     if (n <= 0) continue;
-    const bool in_smem = n <= kPlanSmemCap;
-    u64* khi = in_smem ? s_hi : a.g_hi + lo;
-    u64* klo = in_smem ? s_lo : a.g_lo + lo;
-    float* sw = in_smem ? s_w : a.wn + lo;  // the wn slots double as scratch
-    int32_t* sdst = in_smem ? s_dst : a.g_idx + lo;
+    // two inlined copies so the shared-memory one compiles to LDS/STS (a
+    // pointer chosen at run time between smem and global would be generic)
+    if (n <= kPlanSmemCap)
+      canon_query<true>(a, q, lo, n, n_tiles, s_hi, s_lo, s_w, s_dst, s_run, &s_wsum);
+    else  // long query: global scratch (the wn slots double as its weight scratch)
+      canon_query<false>(a, q, lo, n, n_tiles, a.g_hi + lo, a.g_lo + lo, a.wn + lo, a.g_idx + lo, s_run, &s_wsum);
+  }
+}
+
+template <bool SMEM>
+__device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_t lo, int n, int n_tiles, u64* khi,
+                                            u64* klo, float* sw, int32_t* sdst, int16_t* s_run, float* s_wsum) {
+  {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const int64_t s = lo + i;
       int c = a.cam[s], l = a.lvl[s];
@@ -226,13 +238,13 @@ __global__ void __launch_bounds__(kPlanThreads) plan_canon_kernel(PlanArgs a) {
     if (threadIdx.x == 0) {
       float ws = 0.0f;
       if (a.normalize) {
-        ws = sequential_sum(sw, n, in_smem);
+        ws = sequential_sum(sw, n, SMEM);
         if (ws == 0.0f) set_status(a.status, MSDA_ZERO_WEIGHT_SUM, q);
       }
-      s_wsum = ws;
+      *s_wsum = ws;
     }
     __syncthreads();
-    const float wsum = s_wsum;
+    const float wsum = *s_wsum;
     const int64_t row_base = (q / a.queries_per_batch) * a.rows_per_batch;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const u64 kh = khi[i], kl = klo[i];
@@ -500,37 +512,55 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
 #pragma unroll
   for (int e = 0; e < VEC / 2; ++e) acch[e] = __float2half2_rn(0.0f);
 
-  for (int i = 0; i < n; ++i) {
-    cp_async_wait<D - 1>();
-    const int bi = ((i >> 5) & 1) * 32 + (i & 31);
-    const float4 iw = s_iw[bi];
-    const float wn = s_wn[bi];
-    const unsigned char* src = ring_ptr + read_off;
-    RawVec<BYTES> cv[4];
+  // two samples per iteration: their shared-memory reads and products overlap;
+  // the accumulation itself stays strictly sequential (i, then i + 1)
+  static_assert(D % 2 == 0, "ring depth must be even");
+  for (int i = 0; i < n; i += 2) {
+    cp_async_wait<D - 2>();  // groups i and i + 1 have landed
+    const bool two = i + 1 < n;
+    const int b0 = ((i >> 5) & 1) * 32 + (i & 31);
+    const int b1 = (((i + 1) >> 5) & 1) * 32 + ((i + 1) & 31);
+    const float4 iw0 = s_iw[b0], iw1 = s_iw[b1];
+    const float wn0 = s_wn[b0], wn1 = s_wn[b1];
+    const uint32_t off1 = (read_off + SM::kSlot == (uint32_t)SM::kCorner) ? 0u : read_off + SM::kSlot;
+    RawVec<BYTES> cv0[4], cv1[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) cv[k] = *reinterpret_cast<const RawVec<BYTES>*>(src + k * 32 * BYTES);
+    for (int k = 0; k < 4; ++k) {
+      cv0[k] = *reinterpret_cast<const RawVec<BYTES>*>(ring_ptr + read_off + k * 32 * BYTES);
+      cv1[k] = *reinterpret_cast<const RawVec<BYTES>*>(ring_ptr + off1 + k * 32 * BYTES);
+    }
     if constexpr (!HALF) {
-      float c[4][VEC];
+      float c0[4][VEC], c1[4][VEC];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) to_f32<T, VEC>(cv[k], c[k]);
-      exact_accumulate<VEC>(accf, c, iw, wn, a.one2, a.nz2);
-    } else {
-      const void* cvp[4] = {&cv[0], &cv[1], &cv[2], &cv[3]};
-      half_accumulate<VEC>(acch, cvp, iw, wn);
-    }
-    const int k = i + D;
-    if (k < n) {
-      if ((k & 31) == 0) {  // entering record batch k/32: publish it, prefetch the next
-        __syncwarp();
-        store_batch((k >> 5) & 1);
-        __syncwarp();
-        load_batch((k >> 5) + 1);
+      for (int k = 0; k < 4; ++k) {
+        to_f32<T, VEC>(cv0[k], c0[k]);
+        to_f32<T, VEC>(cv1[k], c1[k]);
       }
-      issue(k, read_off);  // the slot of sample i (just consumed) takes sample i + D
+      exact_accumulate<VEC>(accf, c0, iw0, wn0, a.one2, a.nz2);
+      if (two) exact_accumulate<VEC>(accf, c1, iw1, wn1, a.one2, a.nz2);
+    } else {
+      const void* p0[4] = {&cv0[0], &cv0[1], &cv0[2], &cv0[3]};
+      const void* p1[4] = {&cv1[0], &cv1[1], &cv1[2], &cv1[3]};
+      half_accumulate<VEC>(acch, p0, iw0, wn0);
+      if (two) half_accumulate<VEC>(acch, p1, iw1, wn1);
     }
-    cp_async_commit();
-    read_off += SM::kSlot;
-    if (read_off == (uint32_t)SM::kCorner) read_off = 0;
+    // refill the two consumed slots with samples i + D and i + D + 1
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int k = i + D + j;
+      if (k < n) {
+        if ((k & 31) == 0) {  // entering record batch k/32: publish it, prefetch the next
+          __syncwarp();
+          store_batch((k >> 5) & 1);
+          __syncwarp();
+          load_batch((k >> 5) + 1);
+        }
+        issue(k, read_off);
+      }
+      cp_async_commit();
+      read_off += SM::kSlot;
+      if (read_off == (uint32_t)SM::kCorner) read_off = 0;
+    }
   }
   cp_async_wait<0>();
 

@@ -10,7 +10,6 @@ nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,clocks.mem,power.limit --format=c
 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
 timeout 1200 python -m pytest tests -m gpu -x -q ${PYTEST_ARGS:-} > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
 timeout 600 python bench.py --steps 20 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
-MSDA_F32_LANE_BYTES=8 timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu --e2e-steps 1 > $OUT/bench_lane8.json 2> $OUT/bench_lane8.err
 timeout 900 python tools/bench_paths.py > $OUT/paths.jsonl 2> $OUT/paths.err; echo "paths rc=$?" >> $OUT/paths.err
 if [ "${NCU:-1}" = "1" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file $OUT/launches.csv \
