@@ -8,8 +8,9 @@
 //                       of features.py:261-263.  When the query arrives grouped
 //                       by (camera, level) — the reference bench generator and
 //                       every dense expansion do — each sample's canonical
-//                       slot is its run start (binary search) plus its rank in
-//                       the run; otherwise a bitonic sort.  Then the sequential
+//                       slot is its run start (a shared-memory table) plus its
+//                       rank in the run (one 64-bit (v, u) compare per run
+//                       member); otherwise a bitonic sort.  Then the sequential
 //                       f32 weight sum in canonical order (features.py:264-269)
 //                       and one 32-B SampleRec + normalised weight per sample,
 //                       scattered to its canonical slot.
@@ -71,12 +72,24 @@ struct PlanArgs {
   DevStatus* status;
 };
 
-__device__ __forceinline__ bool key_gt(u64 ah, u64 al, u64 bh, u64 bl) { return ah > bh || (ah == bh && al > bl); }
+__device__ __forceinline__ float key_weight(u64 lo) { return unord_f32((uint32_t)(lo & 0xffffffffu)); }
 
-// Always-ascending bitonic network over n keys, virtually padded with +inf to
-// the next power of two (a compare with a padded partner is a no-op, so no
-// padding is ever stored).  j is a power of two: index math is shifts/masks.
-__device__ void bitonic_sort(u64* hi, u64* lo, int n) {
+constexpr int kRunTable = 1024;  // tiles whose runs are tabulated in shared memory
+
+// Keys are stored as two words: kt = (tile << 32) | ord(w), kp = (ord(v) << 32)
+// | ord(u), so that inside a (camera, level) run one 64-bit compare of kp
+// orders (v, u); the weight (and then position) only breaks exact ties.
+__device__ __forceinline__ bool canon_gt(u64 at, u64 ap, u64 bt, u64 bp) {
+  const uint32_t ta = (uint32_t)(at >> 32), tb = (uint32_t)(bt >> 32);
+  if (ta != tb) return ta > tb;
+  if (ap != bp) return ap > bp;
+  return (uint32_t)at > (uint32_t)bt;
+}
+
+// Always-ascending bitonic network on (kt, kp) in canonical order, virtually
+// padded with +inf to the next power of two (a compare with a padded partner
+// is a no-op, so no padding is stored); j is a power of two: shifts/masks.
+__device__ void bitonic_sort_canon(u64* kt, u64* kp, int n) {
   int N = 1;
   while (N < n) N <<= 1;
   for (int k = 2; k <= N; k <<= 1) {
@@ -87,12 +100,12 @@ __device__ void bitonic_sort(u64* hi, u64* lo, int n) {
         const int i = ((t >> lj) << (lj + 1)) | (t & (j - 1));
         const int p = flip ? (i ^ (k - 1)) : (i + j);
         if (p < n) {
-          const u64 ih = hi[i], il = lo[i], ph = hi[p], pl = lo[p];
-          if (key_gt(ih, il, ph, pl)) {
-            hi[i] = ph;
-            lo[i] = pl;
-            hi[p] = ih;
-            lo[p] = il;
+          const u64 it = kt[i], ip = kp[i], pt = kt[p], pp = kp[p];
+          if (canon_gt(it, ip, pt, pp)) {
+            kt[i] = pt;
+            kp[i] = pp;
+            kt[p] = it;
+            kp[p] = ip;
           }
         }
       }
@@ -101,67 +114,49 @@ __device__ void bitonic_sort(u64* hi, u64* lo, int n) {
   }
 }
 
-// first index in [0, n) whose tile (hi >> 32) is >= t; keys tile-sorted
-__device__ __forceinline__ int tile_lower_bound(const u64* hi, int n, uint32_t t) {
-  int a = 0, b = n;
-  while (a < b) {
-    const int m = (a + b) >> 1;
-    if ((uint32_t)(hi[m] >> 32) < t) a = m + 1; else b = m;
-  }
-  return a;
-}
-
-__device__ __forceinline__ float key_weight(u64 lo) { return unord_f32((uint32_t)(lo & 0xffffffffu)); }
-
-// Canonicalise one query whose n keys sit in (khi, klo).  On return
-// sdst[i] = canonical slot of key i and sw[slot] = its weight; keys are
-// either untouched (rank path) or sorted in place with sdst[i] = i.
-constexpr int kRunTable = 2048;  // tiles whose run start is tabulated in shared memory
-
-__device__ void canon_slots(int n, int n_tiles, u64* khi, u64* klo, int32_t* sdst, float* sw, int16_t* s_run) {
+// Canonicalise one query's n keys.  On return sdst[i] = canonical slot of key
+// i and sw[slot] = its weight; keys are untouched (rank path) or sorted in
+// place with sdst[i] = i.  s_run holds [start, end) of each tile's run.
+__device__ void canon_slots(int n, int n_tiles, u64* kt, u64* kp, int32_t* sdst, float* sw, int16_t* s_run) {
   bool bad = false;
-  for (int i = threadIdx.x + 1; i < n; i += blockDim.x) bad |= (khi[i] >> 32) < (khi[i - 1] >> 32);
-  bool rank_path = !__syncthreads_or(bad);
-  const bool table = n_tiles <= kRunTable && n <= 32767;
+  for (int i = threadIdx.x + 1; i < n; i += blockDim.x) bad |= (kt[i] >> 32) < (kt[i - 1] >> 32);
+  bool rank_path = !__syncthreads_or(bad) && n_tiles <= kRunTable && n <= 32767;
   if (rank_path) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {  // run heads and tails record their run
+      const uint32_t t = (uint32_t)(kt[i] >> 32);
+      if (i == 0 || (uint32_t)(kt[i - 1] >> 32) != t) s_run[2 * t] = (int16_t)i;
+      if (i == n - 1 || (uint32_t)(kt[i + 1] >> 32) != t) s_run[2 * t + 1] = (int16_t)(i + 1);
+    }
+    __syncthreads();
     bool long_run = false;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      if (i > 0 && (khi[i] >> 32) == (khi[i - 1] >> 32)) continue;  // run heads probe their run
-      const uint32_t t = (uint32_t)(khi[i] >> 32);
-      if (table) s_run[t] = (int16_t)i;
-      long_run |= (tile_lower_bound(khi, n, t + 1) - i) > kRunCap;
+      const uint32_t t = (uint32_t)(kt[i] >> 32);
+      long_run |= (s_run[2 * t + 1] - s_run[2 * t]) > kRunCap;
     }
     rank_path = !__syncthreads_or(long_run);
   }
   if (rank_path) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const u64 ih = khi[i], il = klo[i];
-      const uint32_t t = (uint32_t)(ih >> 32);
-      const int rs = table ? (int)s_run[t] : tile_lower_bound(khi, n, t);
-      // inside a run the order is (v, u) as one 64-bit key, then weight, then position
-      const u64 pi = (ih << 32) | (il >> 32);
-      const uint32_t wi = (uint32_t)il;
+      const u64 it = kt[i], ip = kp[i];
+      const uint32_t t = (uint32_t)(it >> 32);
+      const int rs = s_run[2 * t], re = s_run[2 * t + 1];
       int rank = 0;
-      for (int j = rs; j < n; ++j) {
-        const u64 jh = khi[j];
-        if ((uint32_t)(jh >> 32) != t) break;
-        const u64 jl = klo[j];
-        const u64 pj = (jh << 32) | (jl >> 32);
-        if (pj < pi) {
-          ++rank;
-        } else if (pj == pi) {
-          const uint32_t wj = (uint32_t)jl;
-          rank += (wj < wi || (wj == wi && j < i)) ? 1 : 0;
+      for (int j = rs; j < re; ++j) {
+        const u64 jp = kp[j];
+        rank += jp < ip ? 1 : 0;
+        if (jp == ip) {  // exact (v, u) tie: weight, then position
+          const uint32_t wj = (uint32_t)kt[j], wi = (uint32_t)it;
+          rank += (j != i && (wj < wi || (wj == wi && j < i))) ? 1 : 0;
         }
       }
       sdst[i] = rs + rank;
-      sw[rs + rank] = key_weight(il);
+      sw[rs + rank] = key_weight(it);
     }
   } else {
-    bitonic_sort(khi, klo, n);
+    bitonic_sort_canon(kt, kp, n);
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       sdst[i] = i;
-      sw[i] = key_weight(klo[i]);
+      sw[i] = key_weight(kt[i]);
     }
   }
   __syncthreads();
@@ -199,7 +194,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_canon_kernel(PlanArgs a) {
   __shared__ __align__(16) u64 s_lo[kPlanSmemCap];
   __shared__ __align__(16) float s_w[kPlanSmemCap];
   __shared__ __align__(16) int32_t s_dst[kPlanSmemCap];
-  __shared__ int16_t s_run[kRunTable];
+  __shared__ int16_t s_run[2 * kRunTable];
   __shared__ float s_wsum;
   const int n_tiles = a.n_cams * a.n_levels;
 
@@ -230,8 +225,8 @@ __device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_
         l = 0;
       }
       if (!(isfinite(uu) && isfinite(vv) && isfinite(ww))) set_status(a.status, MSDA_NONFINITE, s);
-      khi[i] = ((u64)(c * a.n_levels + l) << 32) | ord_f32(vv);
-      klo[i] = ((u64)ord_f32(uu) << 32) | ord_f32(ww);
+      khi[i] = ((u64)(c * a.n_levels + l) << 32) | ord_f32(ww);  // kt: tile, weight
+      klo[i] = ((u64)ord_f32(vv) << 32) | ord_f32(uu);            // kp: v, u
     }
     __syncthreads();
     canon_slots(n, n_tiles, khi, klo, sdst, sw, s_run);
@@ -247,12 +242,12 @@ __device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_
     const float wsum = *s_wsum;
     const int64_t row_base = (q / a.queries_per_batch) * a.rows_per_batch;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const u64 kh = khi[i], kl = klo[i];
+      const u64 kt = khi[i], kp = klo[i];
       const int dst = sdst[i];
-      const int t = (int)(kh >> 32);
-      const float vv = unord_f32((uint32_t)(kh & 0xffffffffu));
-      const float uu = unord_f32((uint32_t)(kl >> 32));
-      const float ww = key_weight(kl);
+      const int t = (int)(kt >> 32);
+      const float vv = unord_f32((uint32_t)(kp >> 32));
+      const float uu = unord_f32((uint32_t)(kp & 0xffffffffu));
+      const float ww = key_weight(kt);
       const int tt = t < n_tiles ? t : 0;
       a.rec[lo + dst] = make_record(uu, vv, row_base + a.start[tt], a.shape[2 * tt], a.shape[2 * tt + 1]);
       a.wn[lo + dst] = a.normalize ? __fdiv_rn(ww, wsum) : ww;
