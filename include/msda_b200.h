@@ -152,6 +152,17 @@ int32_t msda_oae_pool(const msda_features_t *feat, int32_t n_queries, const floa
                       size_t workspace_bytes, void *stream);
 size_t msda_oae_workspace_size(int32_t n_queries, int32_t n_cams, int32_t channels);
 
+/* Visible fraction of every object in every camera (visibility.py:46-115):
+ * objects [n_objects, 7] f64 (x, y, z, w, l, h, yaw), image_wh [n_cams, 2]
+ * int32, grid samples per axis (reference default 64).  Out: visibility
+ * [n_cams, n_objects] f32 in [0, 1], fully_behind [n_cams, n_objects] (no box
+ * corner in front of the camera -> visibility 0).  These are the v_i that
+ * msda_oae_pool consumes.                                                   */
+size_t msda_visibility_workspace_size(int32_t n_cams, int32_t n_objects);
+int32_t msda_visibility(const msda_cameras_t *cams, const int32_t *image_wh, int32_t n_cams,
+                        const double *objects, int32_t n_objects, int32_t grid, float *visibility,
+                        uint8_t *fully_behind, void *workspace, size_t workspace_bytes, void *stream);
+
 /* Data-dependent status of the last call that used `workspace` (synchronises
  * `stream`).  detail = offending query / sample index, or -1.               */
 int32_t msda_read_status(const void *workspace, void *stream, int32_t *status, int64_t *detail);

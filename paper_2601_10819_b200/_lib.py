@@ -62,6 +62,8 @@ SIGNATURES = {
     "msda_oae_pool": (I32, [ctypes.POINTER(Features), I32, P, I32, P, ctypes.POINTER(Cameras), P, P, P, P, P, P,
                             P, SZ, P]),
     "msda_oae_workspace_size": (SZ, [I32, I32, I32]),
+    "msda_visibility_workspace_size": (SZ, [I32, I32]),
+    "msda_visibility": (I32, [ctypes.POINTER(Cameras), P, I32, P, I32, I32, P, P, P, SZ, P]),
     "msda_read_status": (I32, [P, P, ctypes.POINTER(I32), ctypes.POINTER(I64)]),
     "msda_context_create": (I32, [I32, ctypes.POINTER(P)]),
     "msda_context_destroy": (None, [P]),

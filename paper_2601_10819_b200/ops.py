@@ -297,3 +297,29 @@ def oae_pool(feats: DeviceFeatures, anchors, learned_offsets, cameras: Cameras, 
                              ws.numel(), _stream(dev))
     _check_call(code, ws, dev, check, "oae_pool")
     return out, occl.bool()
+
+
+def visibility(cameras: Cameras, image_wh, objects, grid: int = 64):
+    """Visible fraction of every object in every camera (visibility.py:46-115).
+
+    ``objects`` [n, 7] (x, y, z, w, l, h, yaw); ``image_wh`` [cams, 2].
+    Returns (visibility [cams, n] f32, fully_behind [cams, n] bool).
+    """
+    dev = cameras.K.device
+    obj = torch.as_tensor(objects, dtype=torch.float64).reshape(-1, 7).to(dev).contiguous()
+    wh = torch.as_tensor(image_wh, dtype=torch.int32).reshape(-1, 2).to(dev).contiguous()
+    n_cams, n_obj = int(cameras.K.shape[0]), int(obj.shape[0])
+    if wh.shape[0] != n_cams:
+        raise ValueError("one image size per camera")
+    if grid < 2:
+        raise ValueError("grid must be at least 2")
+    vis = torch.empty((n_cams, n_obj), dtype=torch.float32, device=dev)
+    behind = torch.empty((n_cams, n_obj), dtype=torch.uint8, device=dev)
+    lib = L.lib()
+    ws = WORKSPACE.get(dev, lib.msda_visibility_workspace_size(n_cams, n_obj))
+    cd = cameras.descriptor()
+    code = lib.msda_visibility(ctypes.byref(cd), _ptr(wh), n_cams, _ptr(obj), n_obj, int(grid), _ptr(vis),
+                               _ptr(behind), _ptr(ws), ws.numel(), _stream(dev))
+    if code != L.MSDA_OK:
+        raise_for_status(code, -1, "visibility")
+    return vis, behind.bool()

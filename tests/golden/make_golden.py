@@ -223,8 +223,64 @@ def oae_cases():
             "memory": np.array(mem), "emb": np.array(embs), "occluded": np.array(occl), "views": np.array(views)}
 
 
+def fpyr_case():
+    """A small FPYR container written by the reference writer."""
+    import tempfile
+
+    from mvtrack3d.simulator import write_pyramid_sequence
+
+    rng = np.random.default_rng(47)
+    frames = []
+    for f in range(3):
+        frame = {}
+        for cam in (7, 2):  # unsorted ids: the container sorts them
+            lv = [F.FeatureGrid(stride=8.0 * 2 ** m, values=rng.standard_normal((5 - m, 6 - m, 4)).astype(np.float32))
+                  for m in range(2)]
+            frame[cam] = F.FeaturePyramid(cam, lv)
+        frames.append(frame)
+    with tempfile.TemporaryDirectory() as d:
+        path = Path(d) / "pyr.bin"
+        write_pyramid_sequence(path, frames)
+        blob = np.frombuffer(path.read_bytes(), dtype=np.uint8)
+    return {"blob": blob}
+
+
+def visibility_case():
+    """visible_fraction for every (camera, object) of random ring scenes."""
+    from mvtrack3d.visibility import visible_fraction
+
+    rng = np.random.default_rng(53)
+    scenes = []
+    for k in range(4):
+        cams = ring_cameras(3 + k, size=(640, 480), focal=400.0)
+        objs = []
+        for _ in range(6 + 2 * k):
+            objs.append([rng.uniform(-5, 5), rng.uniform(-5, 5), rng.uniform(0.5, 1.5), rng.uniform(0.4, 1.5),
+                         rng.uniform(0.4, 2.0), rng.uniform(0.8, 2.0), rng.uniform(-math.pi, math.pi)])
+        if k == 1:
+            objs.append([12.0 * math.cos(0.0), 0.0, 4.2, 0.5, 0.5, 0.5, 0.0])  # at camera 0: partly/fully behind
+        states = [G.ObjectState3D(*o) for o in objs]
+        vis = np.zeros((len(cams), len(states)))
+        behind = np.zeros((len(cams), len(states)), dtype=bool)
+        for ci, cam in enumerate(cams):
+            for oi, st in enumerate(states):
+                sc = visible_fraction(cam, st, states, grid=64)
+                vis[ci, oi] = sc.value
+                behind[ci, oi] = sc.fully_behind
+        scenes.append((cams, objs, vis, behind))
+    out = {}
+    for k, (cams, objs, vis, behind) in enumerate(scenes):
+        out[f"K{k}"] = np.array([[c.focal_x, c.focal_y, c.principal_x, c.principal_y] for c in cams])
+        out[f"R{k}"] = np.array([c.rotation for c in cams])
+        out[f"t{k}"] = np.array([c.translation for c in cams])
+        out[f"obj{k}"] = np.array(objs)
+        out[f"vis{k}"] = vis
+        out[f"behind{k}"] = behind
+    return out
+
+
 def main():
-    jobs = [("crit1", crit1), ("features", features_cases), ("bench", bench_cases), ("dense", dense_cases),
+    jobs = [("visibility", visibility_case), ("fpyr", fpyr_case), ("crit1", crit1), ("features", features_cases), ("bench", bench_cases), ("dense", dense_cases),
             ("projection", projection_cases), ("oae", oae_cases)]
     only = set(sys.argv[1:])
     for name, fn in jobs:
