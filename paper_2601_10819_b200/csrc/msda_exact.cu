@@ -434,7 +434,7 @@ struct PipeSmem {
   static constexpr int kPerWarp = kCorner + kRows + kIw + kWn;
 };
 
-constexpr int kPipeWarps = 2;
+constexpr int kPipeWarps = 1;  // one warp per CTA: finest shared-memory granularity per SM
 
 template <typename T, int VEC, bool HALF, int D>
 __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs a) {
@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
 
   // two samples per iteration: their shared-memory reads and products overlap;
   // the accumulation itself stays strictly sequential (i, then i + 1)
-  static_assert(D % 2 == 0, "ring depth must be even");
+  static_assert(D >= 2, "ring depth");
   for (int i = 0; i < n; i += 2) {
     cp_async_wait<D - 2>();  // groups i and i + 1 have landed
     const bool two = i + 1 < n;
@@ -601,8 +601,8 @@ cudaError_t launch_gather_pipe(const GatherArgs& g, cudaStream_t stream) {
 template <typename T, int VEC, bool HALF>
 cudaError_t launch_gather(const GatherArgs& g, cudaStream_t stream) {
   if ((g.C / VEC) % 32 == 0 && g.C % VEC == 0) {
-    if constexpr (VEC * sizeof(T) == 16) return launch_gather_pipe<T, VEC, HALF, 6>(g, stream);
-    else return launch_gather_pipe<T, VEC, HALF, 8>(g, stream);
+    if constexpr (VEC * sizeof(T) == 16) return launch_gather_pipe<T, VEC, HALF, 7>(g, stream);
+    else return launch_gather_pipe<T, VEC, HALF, 12>(g, stream);
   }
   const int lanes = g.C / VEC;
   const int64_t threads = g.n_queries * lanes;
