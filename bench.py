@@ -348,7 +348,8 @@ def run_ours(args, cfg, rank, local_rank, world):
         "stage_us": {"plan_canon": float(np.mean(plan_ms)) * 1e3, "gather_exact": g_ms * 1e3},
         "streams_at_30fps_6layers": int(world * wl.cameras / (30 * 6 * ms_per_step / 1e3)),
         "call_gbs": call_gbs,
-        "roofline": {"bound": "hbm", "kernel": "gather_exact_kernel<float,4>", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": "gather_pipe_kernel<float,4> (exact gather)", "achieved": achieved,
+                     "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(args.config),
                      "peak_source": peak_src, "algorithmic_bytes": ab},
         "e2e": {"value": world * wl.cameras / e2e_s, "unit": "camera-frames/s", "h2d_bytes_per_step": int(h2d),
