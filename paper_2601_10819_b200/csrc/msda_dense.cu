@@ -229,44 +229,6 @@ __global__ void __launch_bounds__(kDenseThreads) dense_fast_kernel(DenseArgs a) 
 constexpr int kWcWarps = 4;
 constexpr int kWcMaxGroups = 32;
 
-template <int NV>
-struct Row {
-  uint4 v[NV];
-};
-
-template <int NV>
-__device__ __forceinline__ Row<NV> ld_row(const char* p) {
-  Row<NV> r;
-#pragma unroll
-  for (int i = 0; i < NV; ++i)
-    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.v[i].x), "=r"(r.v[i].y), "=r"(r.v[i].z), "=r"(r.v[i].w)
-                 : "l"(p + 16 * i));
-  return r;
-}
-
-// VEC stored elements (packed in 32-bit words) -> f32, exact
-template <typename T, int VEC>
-__device__ __forceinline__ void raw_to_f32(const uint32_t* raw, float* f) {
-  if constexpr (sizeof(T) == 4) {
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) f[e] = __uint_as_float(raw[e]);
-  } else if constexpr (std::is_same<T, __half>::value) {
-#pragma unroll
-    for (int e = 0; e < VEC / 2; ++e) {
-      const float2 p = __half22float2(*reinterpret_cast<const __half2*>(&raw[e]));
-      f[2 * e] = p.x;
-      f[2 * e + 1] = p.y;
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < VEC / 2; ++e) {  // bf16 -> f32 is a 16-bit shift
-      f[2 * e] = __uint_as_float(raw[e] << 16);
-      f[2 * e + 1] = __uint_as_float(raw[e] & 0xffff0000u);
-    }
-  }
-}
-
 template <typename T, int VEC, bool PROJECT, bool HACC>
 __global__ void __launch_bounds__(kWcWarps * 32) dense_warpcam_kernel(DenseArgs a) {
   constexpr int NV = VEC * (int)sizeof(T) / 16;

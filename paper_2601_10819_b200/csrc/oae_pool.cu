@@ -9,8 +9,10 @@
 //     a = softmax_k(desc . g_k / sqrt(D)); view = sum_k a_k g_k (oae.py:117-122)
 //   fused = sum_c v_c view_c / sum_c v_c over valid views    (oae.py:125-151)
 //   |fused|_2 normalised; sum v <= 1e-3 -> memory, all_occluded (oae.py:154-164)
-// Threads own VEC consecutive channels (16-B gathers of channel-last rows);
-// g_k lives in shared memory in f64, dot products are block reductions.
+// oae_warp_kernel (below) is the production kernel; oae_pool_kernel is the
+// generic fallback (threads own VEC consecutive channels, g_k staged in f64
+// shared memory, block-reduced dot products) for channel counts that do not
+// fill one warp row.
 #include <algorithm>
 
 #include "msda_common.cuh"
@@ -168,6 +170,167 @@ __global__ void oae_pool_kernel(OaeArgs a) {
   if (threadIdx.x == 0) a.occluded[q] = 0;
 }
 
+// ---------------------------------------------------------------------------
+// Production shape (C == 32 * VEC): one CTA of kOaeWarps warps per query, warp
+// w takes cameras w, w + kOaeWarps, ...; a whole warp covers the channel row.
+// Per valid keypoint the 4 levels x 4 corner rows are loaded together, the
+// level mean and the descriptor score (warp all-reduce) follow, and the
+// keypoint softmax is accumulated online (running max / sum in f64, weighted
+// vector in f32), so no keypoint features are staged.  Per-warp camera partials are
+// summed across warps at the end (tolerance-level reassociation of Eq. 2).
+
+constexpr int kOaeWarps = 8;
+constexpr int kOaeLevels = 4;  // levels loaded together (more are looped)
+
+template <typename T, int VEC>
+__global__ void __launch_bounds__(kOaeWarps * 32, 2) oae_warp_kernel(OaeArgs a) {
+  constexpr int NV = VEC * (int)sizeof(T) / 16;
+  constexpr int LV = NV >= 2 ? 2 : kOaeLevels;  // levels in flight: bounded by registers
+  __shared__ double s_kp[kOaeMaxPoints * 3];
+  __shared__ float s_fused[kOaeWarps][32 * VEC];
+  __shared__ double s_vt[kOaeWarps];
+  __shared__ double s_red[kOaeWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = blockIdx.x;
+  const int c0 = lane * VEC;
+  const size_t row_bytes = (size_t)a.C * sizeof(T);
+  const char* feat = reinterpret_cast<const char*>(a.feat) + (size_t)c0 * sizeof(T);
+
+  for (int p = threadIdx.x; p < a.P; p += blockDim.x)
+    if (!anchor_keypoint(a.anchors + (int64_t)q * 10, p, a.offsets, 0.0f, s_kp + 3 * p))
+      set_status(a.status, MSDA_OFFSET_RANGE, p);
+  __syncthreads();
+
+  float d[VEC], fused[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    d[e] = a.desc[(int64_t)q * a.C + c0 + e];
+    fused[e] = 0.0f;
+  }
+  const double inv_sqrt_d = 1.0 / sqrt((double)a.C);
+  double vt = 0.0;
+
+  for (int cam = warp; cam < a.cams; cam += kOaeWarps) {
+    double up = 0.0, vp = 0.0;
+    const bool ok = lane < a.P &&
+                    project_f64(a.K + cam * 4, a.R + cam * 9, a.T + cam * 3, s_kp + 3 * min(lane, a.P - 1), up, vp);
+    unsigned mask = __ballot_sync(0xffffffffu, ok);
+    if (mask == 0u) continue;  // every keypoint behind: invalid view, zero weight (oae.py:114-115, 141-143)
+    double m = -INFINITY, z = 0.0;
+    float acc[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) acc[e] = 0.0f;
+    while (mask) {
+      const int p = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const double u = __shfl_sync(0xffffffffu, up, p), v = __shfl_sync(0xffffffffu, vp, p);
+      float g[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) g[e] = 0.0f;
+      for (int l0 = 0; l0 < a.L; l0 += LV) {
+        SampleRec r[LV];
+        Row<NV> c[LV][4];
+#pragma unroll
+        for (int j = 0; j < LV; ++j) {
+          const int l = l0 + j;
+          if (l < a.L) {
+            const int t = cam * a.L + l;
+            const double st = (double)a.strides[l];
+            r[j] = make_record((float)(u / st - 0.5), (float)(v / st - 0.5), a.start[t], a.shape[2 * t],
+                               a.shape[2 * t + 1]);
+          } else {
+            r[j].row[0] = r[j].row[1] = r[j].row[2] = r[j].row[3] = -1;
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (r[j].row[k] >= 0) c[j][k] = ld_row<NV>(feat + (size_t)r[j].row[k] * row_bytes);
+            else
+#pragma unroll
+              for (int i = 0; i < NV; ++i) c[j][k].v[i] = make_uint4(0, 0, 0, 0);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < LV; ++j) {
+          if (l0 + j >= a.L) break;
+          float f[4][VEC];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) raw_to_f32<T, VEC>(reinterpret_cast<const uint32_t*>(c[j][k].v), f[k]);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {  // reference f32 bilinear tree (features.py:219)
+            const float b = __fadd_rn(__fadd_rn(__fmul_rn(f[0][e], r[j].iw[0]), __fmul_rn(f[1][e], r[j].iw[1])),
+                                      __fadd_rn(__fmul_rn(f[2][e], r[j].iw[2]), __fmul_rn(f[3][e], r[j].iw[3])));
+            g[e] += b;
+          }
+        }
+      }
+      double dot = 0.0;
+      const float inv_l = 1.0f / (float)a.L;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        g[e] *= inv_l;  // level mean (oae.py:112)
+        dot += (double)g[e] * (double)d[e];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      const double s = dot * inv_sqrt_d;
+      const double m2 = fmax(m, s);
+      const double scale = exp(m - m2), w = exp(s - m2);  // online softmax (oae.py:117-122)
+      z = z * scale + w;
+      const float fs = (float)scale, fw = (float)w;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc[e] = acc[e] * fs + fw * g[e];
+      m = m2;
+    }
+    const double vis = (double)a.vis[(int64_t)q * a.cams + cam];
+    vt += vis;
+    const float vz = (float)(vis / z);
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) fused[e] += vz * acc[e];
+  }
+
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) s_fused[warp][c0 + e] = fused[e];
+  if (lane == 0) s_vt[warp] = vt;
+  __syncthreads();
+  double total = 0.0;
+#pragma unroll
+  for (int w = 0; w < kOaeWarps; ++w) total += s_vt[w];
+  float* o = a.out + (int64_t)q * a.C;
+  if (!(total > 1e-3)) {  // AllOccluded -> keep the memory embedding (oae.py:159-164)
+    for (int c = threadIdx.x; c < a.C; c += blockDim.x) o[c] = a.memory[(int64_t)q * a.C + c];
+    if (threadIdx.x == 0) a.occluded[q] = 1;
+    return;
+  }
+  // fused / total, then L2 normalise (oae.py:151, 44-50)
+  double sq = 0.0;
+  for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
+    double f = 0.0;
+#pragma unroll
+    for (int w = 0; w < kOaeWarps; ++w) f += (double)s_fused[w][c];
+    f /= total;
+    s_fused[0][c] = (float)f;  // each c is owned by one thread: safe in place after the sum
+    sq += f * f;
+  }
+#pragma unroll
+  for (int o2 = 16; o2 > 0; o2 >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o2);
+  if (lane == 0) s_red[warp] = sq;
+  __syncthreads();
+  double norm2 = 0.0;
+#pragma unroll
+  for (int w = 0; w < kOaeWarps; ++w) norm2 += s_red[w];
+  const double norm = sqrt(norm2);
+  if (!(norm >= 1e-12)) set_status(a.status, MSDA_BAD_ARG, q);
+  for (int c = threadIdx.x; c < a.C; c += blockDim.x) o[c] = (float)((double)s_fused[0][c] / norm);
+  if (threadIdx.x == 0) a.occluded[q] = 0;
+}
+
+template <typename T, int VEC>
+cudaError_t launch_oae_warp(const OaeArgs& a, cudaStream_t s) {
+  if (a.Q == 0) return cudaSuccess;
+  oae_warp_kernel<T, VEC><<<a.Q, kOaeWarps * 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <typename T, int VEC>
 cudaError_t launch_oae_t(const OaeArgs& a, cudaStream_t s) {
   const int lanes = a.C / VEC;
@@ -235,9 +398,15 @@ int32_t msda_oae_pool(const msda_features_t* f, int32_t n_queries, const float* 
   const uintptr_t al = reinterpret_cast<uintptr_t>(f->data);
   cudaError_t e;
   const int C = f->channels;
+  const bool al16 = al % 16 == 0;
+  if (al16 && f->dtype == MSDA_F32 && C == 256) return launch_oae_warp<float, 8>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
+  if (al16 && f->dtype == MSDA_F32 && C == 128) return launch_oae_warp<float, 4>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
+  if (al16 && f->dtype == MSDA_F16 && C == 256) return launch_oae_warp<__half, 8>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
+  if (al16 && f->dtype == MSDA_BF16 && C == 256)
+    return launch_oae_warp<__nv_bfloat16, 8>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
   switch (f->dtype) {
     case MSDA_F32:
-      e = (C % 4 == 0 && al % 16 == 0) ? launch_oae_t<float, 4>(a, s) : launch_oae_t<float, 2>(a, s);
+      e = (C % 4 == 0 && al16) ? launch_oae_t<float, 4>(a, s) : launch_oae_t<float, 2>(a, s);
       break;
     case MSDA_F16:
       e = (C % 8 == 0 && al % 16 == 0) ? launch_oae_t<__half, 8>(a, s) : launch_oae_t<__half, 2>(a, s);

@@ -220,3 +220,48 @@ def test_oae_channel_mismatch(cuda_dev):
     with pytest.raises(ChannelMismatch):
         ops.oae_pool(feats, torch.zeros(1, 10), np.zeros((0, 3)), camd, [8.0], torch.zeros(1, 6), torch.ones(1, 1),
                      torch.zeros(1, 4))
+
+
+@pytest.mark.parametrize("dt", ["float32", "bfloat16"])
+def test_oae_pool_production_kernel(cuda_dev, dt):
+    """C = 256 takes the warp-per-camera online-softmax kernel; compare with
+    the oracle (oae.py:81-164 restated) on the features the GPU sees."""
+    import torch
+
+    from paper_2601_10819_b200 import ops
+
+    rng = np.random.default_rng(61)
+    cams, n_levels, channels = 10, 4, 256
+    strides = [4.0, 8.0, 16.0, 32.0]
+    grids, shape = {}, np.zeros((cams, n_levels, 2), dtype=np.int32)
+    for c in range(cams):
+        for m, s in enumerate(strides):
+            h, w = int(math.ceil(256 / s)), int(math.ceil(704 / s))
+            grids[(c, m)] = rng.uniform(-1, 1, (h, w, channels)).astype(np.float32)
+            shape[c, m] = (h, w)
+    feats, table, tiles = _feats(ops, torch, grids, shape, cuda_dev, dtype=getattr(torch, dt))
+    seen = feats.table[0].float().cpu().numpy()
+    K, R, T = _ring(cams)
+    camd = ops.Cameras(K, R, T, device=cuda_dev)
+    q_n = 12
+    anchors = np.zeros((q_n, 10), dtype=np.float32)
+    anchors[:, 0:2] = rng.uniform(-4, 4, (q_n, 2))
+    anchors[:, 2] = 0.9
+    anchors[:, 3:6] = (0.6, 0.6, 1.8)
+    anchors[:, 6] = rng.uniform(-math.pi, math.pi, q_n)
+    offsets = rng.uniform(-1, 1, (6, 3)).astype(np.float32)
+    desc = rng.standard_normal((q_n, channels)).astype(np.float32)
+    vis = rng.uniform(0.0, 1.0, (q_n, cams)).astype(np.float32)
+    vis[4] = 1e-5  # all occluded -> memory
+    mem = rng.standard_normal((q_n, channels)).astype(np.float32)
+    mem /= np.linalg.norm(mem, axis=1, keepdims=True)
+    t = lambda a: torch.from_numpy(a).to(cuda_dev)  # noqa: E731
+    emb, occl = ops.oae_pool(feats, t(anchors), offsets, camd, strides, t(desc), t(vis), t(mem))
+    emb, occl = emb.cpu().numpy(), occl.cpu().numpy()
+    for q in range(q_n):
+        kps = mo.keypoints(anchors[q].astype(np.float64), offsets.astype(np.float64))
+        views = [mo.extract_view(seen, tiles, n_levels, c, strides, K[c], R[c], T[c], kps, desc[q].astype(np.float64))
+                 for c in range(cams)]
+        ref, ref_occ = mo.fuse(views, vis[q], mem[q])
+        assert bool(occl[q]) == ref_occ
+        assert np.abs(emb[q] - ref).max() <= 1e-4, q
