@@ -265,3 +265,41 @@ def test_oae_pool_production_kernel(cuda_dev, dt):
         ref, ref_occ = mo.fuse(views, vis[q], mem[q])
         assert bool(occl[q]) == ref_occ
         assert np.abs(emb[q] - ref).max() <= 1e-4, q
+
+
+def _uniform_grids(rng, cams, levels, channels):
+    grids = {}
+    shape = np.zeros((cams, len(levels), 2), dtype=np.int32)
+    for c in range(cams):
+        for m, (h, w) in enumerate(levels):
+            grids[(c, m)] = rng.uniform(-1, 1, (h, w, channels)).astype(np.float32)
+            shape[c, m] = (h, w)
+    return grids, shape
+
+
+@pytest.mark.parametrize("dt,precision,normalize,channels,groups", [
+    ("float32", "fast", False, 256, 8), ("float32", "fast", True, 256, 8), ("float32", "fast", False, 128, 4),
+    ("float16", "fast", False, 256, 8), ("float16", "fast_h2", False, 256, 8), ("bfloat16", "fast", True, 256, 8)])
+def test_dense_slice_kernel(cuda_dev, dt, precision, normalize, channels, groups):
+    """Equal level shapes on every camera select the coarse-level staging
+    kernel (camera x channel-slice CTAs, red.add partials)."""
+    import torch
+
+    from paper_2601_10819_b200 import ops
+
+    rng = np.random.default_rng(71)
+    cams, levels = 5, [(32, 88), (16, 44), (8, 22), (4, 11)]
+    grids, shape = _uniform_grids(rng, cams, levels, channels)
+    feats, table, tiles = _feats(ops, torch, grids, shape, cuda_dev, dtype=getattr(torch, dt), batch=2)
+    seen = feats.table[0].float().cpu().numpy()
+    bs, q_n, p_n = 2, 40, 13
+    loc = rng.uniform(-0.05, 1.05, (bs, q_n, p_n, cams, 2)).astype(np.float32)
+    logits = rng.standard_normal((bs, q_n, p_n * cams * 4, groups))
+    e = np.exp(logits - logits.max(axis=2, keepdims=True))
+    wts = (e / e.sum(axis=2, keepdims=True)).reshape(bs, q_n, p_n, cams, 4, groups).astype(np.float32)
+    t = lambda a: torch.from_numpy(a).to(cuda_dev)  # noqa: E731
+    out = ops.deformable_aggregation(feats, None, None, t(loc), t(wts), precision=precision, normalize=normalize,
+                                     check=True).cpu().numpy()
+    ref = mo.msda_dense_groups(seen, tiles, shape, loc, wts, 4, normalize=normalize)
+    tol = 1e-2 if precision == "fast_h2" else 1e-4
+    assert rel(out, ref) <= tol
