@@ -374,18 +374,104 @@ def run_ours(args, cfg, rank, local_rank, world):
         dist.destroy_process_group()
 
 
+DENSE_CONFIGS = {
+    # cfg5 (BASELINE configs[4]): 512 cameras of the cfg1 per-camera shape, fp16, Sparse4D dense FAST path
+    "cfg5-stream": dict(cams=512, scene=32, shard="stream",
+                        desc="512 cams as 16 scenes x 32 cams, fp16, dense FAST, scenes dealt round-robin to ranks"),
+    "cfg5-camera": dict(cams=512, scene=512, shard="camera",
+                        desc="one 512-cam scene, fp16, dense FAST, cameras split across ranks + NCCL partial-sum "
+                             "all-reduce of [Q, C]"),
+}
+CFG1_LEVELS = [(64, 176), (32, 88), (16, 44), (8, 22)]
+
+
+def run_dense_scaling(args, cfg, rank, local_rank, world):
+    """cfg5 sweep (strong scaling: 512 cameras in total whatever N is)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_10819_b200 import ops
+    from paper_2601_10819_b200.dist import CameraShardedAggregation, camera_range, shard_streams
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    Q, P, G, C, L = 900, 13, 8, 256, 4
+    gen = torch.Generator(device=dev).manual_seed(rank)
+
+    def scene_feats(n_cams):
+        rows = n_cams * sum(h * w for h, w in CFG1_LEVELS)
+        table = (torch.rand((1, rows, C), generator=gen, device=dev) * 2 - 1).half()
+        shape = torch.tensor([[list(x) for x in CFG1_LEVELS]] * n_cams, dtype=torch.int32)
+        start = torch.tensor([[c * rows // n_cams + sum(h * w for h, w in CFG1_LEVELS[:m]) for m in range(L)]
+                              for c in range(n_cams)], dtype=torch.int64)
+        return ops.DeviceFeatures(table, shape, start)
+
+    def inputs(n_cams):
+        loc = torch.rand((1, Q, P, n_cams, 2), generator=gen, device=dev)
+        w = torch.softmax(torch.randn((1, Q, P * n_cams * L, G), generator=gen, device=dev), dim=2)
+        return loc, w.reshape(1, Q, P, n_cams, L, G).contiguous()
+
+    if cfg["shard"] == "stream":
+        mine = shard_streams(cfg["cams"] // cfg["scene"], rank, world)
+        work = [(scene_feats(cfg["scene"]), *inputs(cfg["scene"])) for _ in mine]
+
+        def step():
+            for f, loc, w in work:
+                ops.deformable_aggregation(f, None, None, loc, w, precision="fast")
+    else:
+        lo, hi = camera_range(cfg["cams"], rank, world)
+        feats = scene_feats(hi - lo)
+        loc, w = inputs(hi - lo)  # this rank's cameras of the scene's sampling plan
+        agg = CameraShardedAggregation.for_device_features(cfg["cams"], feats, precision="fast")
+
+        def step():
+            agg(loc, w, local_inputs=True)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(args.steps):
+        step()
+    b.record()
+    torch.cuda.synchronize(dev)
+    ms = a.elapsed_time(b) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": cfg["cams"] / (ms / 1e3), "unit": "camera-frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f16", "data": "synthetic (device RNG)",
+            "config": {"workload": args.config, "desc": cfg["desc"], "queries": Q, "points": P, "groups": G,
+                       "channels": C, "levels": CFG1_LEVELS},
+            "streams_at_30fps_6layers": int(cfg["cams"] / (30 * 6 * ms / 1e3))}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS) + sorted(DENSE_CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank, local_rank, world = dist_env()
+    if args.config in DENSE_CONFIGS:
+        run_dense_scaling(args, DENSE_CONFIGS[args.config], rank, local_rank, world)
+        return
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)

@@ -160,25 +160,46 @@ __global__ void __launch_bounds__(kSliceWarps * 32, 1) dense_slice_kernel(SliceA
         for (int gg = 0; gg < ng; ++gg) s_w[warp][lane * kSliceMaxGroups + gg] = valid ? __ldg(wp + gg) : 0.0f;
       }
       __syncwarp();
-      for (int i = 0; i < n; ++i) {
-        const SampleRec r = s_rec[warp][i];
-        const int l = s_lvl[warp][i];
-        const float wg = s_w[warp][i * kSliceMaxGroups + g_lane];
-        LV c[4];
-        if (l >= a.first_staged) {
-          const unsigned char* lv = smem_raw + a.staged_off[l] + lane * LB;
+      // kUnroll samples per step: all their corner loads are issued before
+      // any of them is consumed (memory-level parallelism per warp)
+      constexpr int kUnroll = 4;
+      for (int i0 = 0; i0 < n; i0 += kUnroll) {
+        SampleRec rr[kUnroll];
+        float wgs[kUnroll];
+        LV cc[kUnroll][4];
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            c[k] = r.row[k] >= 0 ? *reinterpret_cast<const LV*>(lv + (size_t)r.row[k] * SC * esz) : LV{};
-        } else {
+        for (int j = 0; j < kUnroll; ++j) {
+          const int i = i0 + j;
+          if (i >= n) {
+            wgs[j] = 0.0f;
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            c[k] = r.row[k] >= 0 ? __ldg(reinterpret_cast<const LV*>(featc + (size_t)r.row[k] * row_bytes)) : LV{};
+            for (int k = 0; k < 4; ++k) cc[j][k] = LV{};
+            continue;
+          }
+          rr[j] = s_rec[warp][i];
+          wgs[j] = s_w[warp][i * kSliceMaxGroups + g_lane];
+          const int l = s_lvl[warp][i];
+          if (l >= a.first_staged) {
+            const unsigned char* lv = smem_raw + a.staged_off[l] + lane * LB;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              cc[j][k] = rr[j].row[k] >= 0 ? *reinterpret_cast<const LV*>(lv + (size_t)rr[j].row[k] * SC * esz)
+                                           : LV{};
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              cc[j][k] = rr[j].row[k] >= 0
+                             ? __ldg(reinterpret_cast<const LV*>(featc + (size_t)rr[j].row[k] * row_bytes))
+                             : LV{};
+          }
         }
 #pragma unroll
+        for (int j = 0; j < kUnroll; ++j)
+#pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const float cw = r.iw[k] * wg;
-          const uint32_t* raw = reinterpret_cast<const uint32_t*>(&c[k]);
+          if (i0 + j >= n) break;
+          const float cw = rr[j].iw[k] * wgs[j];
+          const uint32_t* raw = reinterpret_cast<const uint32_t*>(&cc[j][k]);
           if constexpr (H2) {
             const __half2 cwh = __float2half2_rn(cw);
 #pragma unroll
@@ -257,6 +278,9 @@ bool plan_slice(const int32_t* shape_host, int cams, int L, int C, int esz, int 
       if (shape_host[2 * L * c + i] != shape_host[i]) return false;
   const int budget = kSliceStageBudget;
   const int cpg = C / G;
+  // the slice width that keeps the most levels on chip wins; ties go to the
+  // widest slice (fewer, larger lane loads)
+  int best_vec = 0, best_fs = L;
   for (int vec : {8, 4, 2}) {
     const int SC = 32 * vec;
     if (C % SC || vec * esz < 4 || vec * esz > 16 || SC % cpg && cpg % SC) continue;
@@ -264,26 +288,28 @@ bool plan_slice(const int32_t* shape_host, int cams, int L, int C, int esz, int 
     // stage from the coarsest level down while it fits
     int bytes = 0, fs = L;
     for (int l = L - 1; l >= 1; --l) {  // never stage level 0 (finest; little reuse)
-      const int cells = shape_host[2 * l] * shape_host[2 * l + 1];
-      const int need = cells * SC * esz;
+      const int need = shape_host[2 * l] * shape_host[2 * l + 1] * SC * esz;
       if (bytes + need > budget) break;
       bytes += need;
       fs = l;
     }
-    if (fs < L) {
-      VEC = vec;
-      first_staged = fs;
-      int off = 0;
-      for (int l = 0; l < kSliceMaxLevels; ++l) staged_off[l] = 0;
-      for (int l = fs; l < L; ++l) {
-        staged_off[l] = off;
-        off += shape_host[2 * l] * shape_host[2 * l + 1] * SC * esz;
-      }
-      stage_bytes = off;
-      return true;
+    if (fs < best_fs) {
+      best_fs = fs;
+      best_vec = vec;
     }
   }
-  return false;
+  if (best_fs >= L) return false;
+  VEC = best_vec;
+  first_staged = best_fs;
+  const int SC = 32 * best_vec;
+  int off = 0;
+  for (int l = 0; l < kSliceMaxLevels; ++l) staged_off[l] = 0;
+  for (int l = best_fs; l < L; ++l) {
+    staged_off[l] = off;
+    off += shape_host[2 * l] * shape_host[2 * l + 1] * SC * esz;
+  }
+  stage_bytes = off;
+  return true;
 }
 
 cudaError_t launch_dense_slice(const msda_features_t& f, int Q, int P, int G, const float* loc, const float* w,

@@ -54,11 +54,15 @@ class CameraShardedAggregation:
         self.world = dist.get_world_size(self.group) if dist.is_initialized() else 1
         self.cam_lo, self.cam_hi = camera_range(self.n_cams, self.rank, self.world)
 
-    def __call__(self, sampling_location, weights, normalize: bool = False):
+    def __call__(self, sampling_location, weights, normalize: bool = False, local_inputs: bool = False):
         """sampling_location [bs, Q, P, cams, 2], weights [bs, Q, P, cams, L, G]
-        for ALL cameras (each rank slices its own); returns [bs, Q, C]."""
-        loc = sampling_location[:, :, :, self.cam_lo:self.cam_hi].contiguous()
-        wts = weights[:, :, :, self.cam_lo:self.cam_hi].contiguous()
+        for ALL cameras (each rank slices its own) or, with ``local_inputs``,
+        already restricted to this rank's camera range; returns [bs, Q, C]."""
+        if local_inputs:
+            loc, wts = sampling_location, weights
+        else:
+            loc = sampling_location[:, :, :, self.cam_lo:self.cam_hi].contiguous()
+            wts = weights[:, :, :, self.cam_lo:self.cam_hi].contiguous()
         part = self.local_fn(loc, wts)
         bs, q_n, c_n = part.shape
         g_n = weights.shape[-1]
