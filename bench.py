@@ -167,11 +167,14 @@ def cpu_reference_time(gw, budget_s=15.0, reps=3, workers=None):
                                gw.vs[:s], gw.weights[:s], precision="full", workers=workers)
         return time.perf_counter() - t0, out
 
-    probe = min(wl.queries, max(2 * workers, 32))
-    t_probe, _ = run(probe)  # warm-up + rate probe
-    per_query = t_probe / probe
-    nq = int(min(wl.queries, max(probe, budget_s / reps / max(per_query, 1e-9))))
-    times, out = [], None
+    # The tile-grouped algorithm has a per-(camera, level) cost that a query
+    # subset does not shrink, so a subset would over-state the full-call time:
+    # time the whole workload unless one call exceeds the per-rep budget.
+    t_full, out = run(wl.queries)  # warm-up and size probe
+    nq = wl.queries
+    if t_full > budget_s / reps:
+        nq = max(2 * workers, int(wl.queries * (budget_s / reps) / t_full))
+    times = []
     for _ in range(reps):
         t, out = run(nq)
         times.append(t)
@@ -186,8 +189,8 @@ def run_reference(args, cfg, rank, world):
     wl = BenchWorkload(**cfg["wl"])
     gw = generate_workload(wl)
     workers = os.cpu_count() or 1
-    # size the per-step sample so warmup+steps finish within ~2 minutes
-    r = cpu_reference_time(gw, budget_s=max(1.0, 100.0 / max(1, args.steps + args.warmup)), reps=1,
+    # full workload per step unless warmup+steps would exceed ~3 minutes
+    r = cpu_reference_time(gw, budget_s=max(1.0, 180.0 / max(1, args.steps + args.warmup)), reps=1,
                            workers=workers)
     nq = r["sample_queries"]
     from oracle import msda_oracle as mo
@@ -205,7 +208,8 @@ def run_reference(args, cfg, rank, world):
         times.append(time.perf_counter() - t0)
     t_full = float(np.mean(times)) * wl.queries / nq
     value = wl.cameras / t_full
-    sample = (f"{nq} of {wl.queries} queries per step ({nq * wl.cameras * wl.levels * wl.points_per_query} "
+    sample = (f"the full workload per step ({wl.num_samples} samples)" if nq == wl.queries else
+              f"{nq} of {wl.queries} queries per step ({nq * wl.cameras * wl.levels * wl.points_per_query} "
               f"samples), extrapolated linearly to the full call")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "camera-frames/s", "n_gpus": world,
@@ -365,7 +369,9 @@ def run_ours(args, cfg, rank, local_rank, world):
         parity = r["out"].tobytes() == out.cpu().numpy()[:nq].tobytes()
         line["cpu_baseline"] = {
             "value": wl.cameras / r["full_call_s"], "unit": "camera-frames/s", "cores": r["workers"],
-            "kind": "port", "sample": f"{nq} of {wl.queries} queries x3 reps (1 warm-up), extrapolated linearly",
+            "kind": "port",
+            "sample": (f"full workload ({wl.num_samples} samples) x3 reps after 1 warm-up" if nq == wl.queries
+                       else f"{nq} of {wl.queries} queries x3 reps (1 warm-up), extrapolated linearly"),
             "algorithm": "oracle msda_tiled (reference msda_optimized FULL restated, numpy, threads)",
             "gpu_bitwise_equal_on_sample": bool(parity)}
     print(json.dumps(line), flush=True)
