@@ -25,7 +25,6 @@
 #include <type_traits>
 
 #include "msda_common.cuh"
-#include "msda_dense_slice.cuh"
 #include "msda_exact.cuh"
 
 namespace msda {
@@ -556,24 +555,6 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
   if (nq == 0) return MSDA_OK;
   if (precision == MSDA_FAST || precision == MSDA_FAST_H2) {
     const bool h2 = precision == MSDA_FAST_H2;
-    // coarse-level staging (camera x channel-slice CTAs) when the level shapes
-    // are known on the host and the coarse levels fit in shared memory
-    int vec = 0, first = 0, stage = 0, offs[8];
-    const int esz = f->dtype == MSDA_F32 ? 4 : 2;
-    static const bool slice_off = [] {
-      const char* e = getenv("MSDA_DENSE_SLICE");
-      return e && e[0] == '0';
-    }();
-    if (!slice_off && f->spatial_shape_host && !(project && normalize) &&
-        plan_slice(f->spatial_shape_host, f->n_cams, f->n_levels, f->channels, esz, G, vec, first, offs, stage)) {
-      int dev = 0, sms = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      const cudaError_t e = launch_dense_slice(*f, Q, P, G, loc, w, project, anchors, offsets, cams, strides, dt,
-                                               h2 && f->dtype == MSDA_F16, normalize, out, ew.status, vec, first,
-                                               offs, stage, sms, s);
-      return e == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
-    }
     const cudaError_t e =
         project ? launch_dense_fast<true>(a, f->dtype, h2, s) : launch_dense_fast<false>(a, f->dtype, h2, s);
     return e == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;

@@ -91,8 +91,6 @@ class DeviceFeatures:
             raise ValueError("spatial_shape must be [cams, levels, 2]")
         if tuple(self.scale_start_index.shape) != tuple(self.spatial_shape.shape[:2]):
             raise ValueError("scale_start_index must be [cams, levels]")
-        self._shape_host = self.spatial_shape.cpu().contiguous()  # lets the library pick shape-tuned kernels
-
     @property
     def n_cams(self):
         return int(self.spatial_shape.shape[0])
@@ -108,7 +106,7 @@ class DeviceFeatures:
     def descriptor(self) -> L.Features:
         return L.Features(_ptr(self.table), _DTYPES[self.table.dtype], int(self.table.shape[0]), self.n_cams,
                           self.n_levels, self.channels, 0, int(self.table.shape[1]), _ptr(self.spatial_shape),
-                          _ptr(self.scale_start_index), _ptr(self._shape_host))
+                          _ptr(self.scale_start_index))
 
     @classmethod
     def from_grids(cls, grids, device="cuda", dtype=torch.float32):
