@@ -163,6 +163,36 @@ int32_t msda_visibility(const msda_cameras_t *cams, const int32_t *image_wh, int
                         const double *objects, int32_t n_objects, int32_t grid, float *visibility,
                         uint8_t *fully_behind, void *workspace, size_t workspace_bytes, void *stream);
 
+/* Feature painting (simulator.py:249-289) straight into
+ * the channel-last table: grid (cam, level) has spatial_shape (H, W) =
+ * (ceil(img_h / stride), ceil(img_w / stride)) (simulator.py:252-253) and
+ * starts at scale_start_index.  entities [n_objects + n_occluders, 7] f64
+ * (x, y, z, w, l, h, yaw): moving objects (signatures [n_objects, C] f64)
+ * then occluders (paint nothing).  A cell takes the signature of the nearest
+ * entity whose projected rect (visibility.py:46-65) covers its centre.
+ * background [rows, C] f64 (the reference's numpy draw: bit-identical
+ * output) or NULL (device Philox N(0, sigma) keyed by seed/frame).
+ * out [rows, C] of out_dtype = f32(background + signature) (then rounded to
+ * f16/bf16).  strides [L] f64, device; spatial_shape_host = host copy.      */
+size_t msda_paint_workspace_size(int32_t n_cams, int32_t n_entities);
+int32_t msda_paint(const msda_cameras_t *cams, int32_t n_cams, int32_t n_levels, const double *strides,
+                   const int32_t *spatial_shape, const int32_t *spatial_shape_host,
+                   const int64_t *scale_start_index, int32_t channels, const double *entities,
+                   int32_t n_objects, int32_t n_occluders, const double *signatures,
+                   const double *background, float sigma, uint64_t seed, int32_t frame, int32_t out_dtype,
+                   void *out, void *workspace, size_t workspace_bytes, void *stream);
+
+/* Tracker association cost (tracker.py:105-142), f64,
+ * bit-identical to the reference's numpy: geo = |c_q - c_d|, emb = |m_q -
+ * e_d| (np.linalg.norm: numpy pairwise summation order), admissible = geo <=
+ * gate_radius, cost = alpha_emb*emb + alpha_geo*geo/gate (gate = 1 when
+ * gate_radius is infinite), solver_cost = admissible ? cost : 1e9.  Centres
+ * [n, 3], embeddings [n, dim] (dim <= 1024), outputs [n_q, n_d], device.   */
+int32_t msda_assoc_cost(const double *q_centers, const double *d_centers, const double *q_embeddings,
+                        const double *d_embeddings, int32_t n_q, int32_t n_d, int32_t dim, double gate_radius,
+                        double alpha_emb, double alpha_geo, double *cost, double *solver_cost,
+                        uint8_t *admissible, void *stream);
+
 /* Data-dependent status of the last call that used `workspace` (synchronises
  * `stream`).  detail = offending query / sample index, or -1.               */
 int32_t msda_read_status(const void *workspace, void *stream, int32_t *status, int64_t *detail);

@@ -64,6 +64,11 @@ SIGNATURES = {
     "msda_oae_workspace_size": (SZ, [I32, I32, I32]),
     "msda_visibility_workspace_size": (SZ, [I32, I32]),
     "msda_visibility": (I32, [ctypes.POINTER(Cameras), P, I32, P, I32, I32, P, P, P, SZ, P]),
+    "msda_paint_workspace_size": (SZ, [I32, I32]),
+    "msda_paint": (I32, [ctypes.POINTER(Cameras), I32, I32, P, P, P, P, I32, P, I32, I32, P, P, ctypes.c_float,
+                         ctypes.c_uint64, I32, I32, P, P, SZ, P]),
+    "msda_assoc_cost": (I32, [P, P, P, P, I32, I32, I32, ctypes.c_double, ctypes.c_double, ctypes.c_double, P, P, P,
+                              P]),
     "msda_read_status": (I32, [P, P, ctypes.POINTER(I32), ctypes.POINTER(I64)]),
     "msda_context_create": (I32, [I32, ctypes.POINTER(P)]),
     "msda_context_destroy": (None, [P]),

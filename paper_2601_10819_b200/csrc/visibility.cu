@@ -136,6 +136,148 @@ __global__ void __launch_bounds__(256) visible_kernel(VisArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Feature painting (simulator.py:249-289): the producer
+// of the pyramids the MSDA path reads, written straight into the
+// channel-last concatenated table (mc_ms_feat) in the compute dtype.
+//   cell centre (x + 0.5) * stride, (y + 0.5) * stride (f64, simulator.py:
+//   275-277); winner = the nearest (strictly smaller mean depth, first in
+//   entity order on ties) rect containing it (closed bounds, visibility.py:
+//   32-33); moving objects add their f64 signature, occluders nothing
+//   (simulator.py:283-288); value = f32(background + signature).
+// The background is the caller's f64 grid (bit-identical to the reference
+// given the reference's numpy draw) or, when absent, drawn on device:
+// Philox4x32-10 (counter = element / 4, tile, frame; key = seed) and a
+// Box-Muller transform — the same N(0, sigma) law, not the same numbers.
+
+struct PaintArgs {
+  const Rect* rects;        // [cams, n_ent]
+  const double* strides;    // [L]
+  const int32_t* shape;     // [cams, L, 2]
+  const int64_t* start;     // [cams, L]
+  const double* sig;        // [n_obj, C]
+  const double* bg;         // [rows, C] or null
+  void* out;                // [rows, C]
+  int32_t cams, L, C, n_ent, n_obj, dtype, frame;
+  float sigma;
+  uint32_t key0, key1;
+};
+
+constexpr int kPaintCells = 64;  // cells per CTA
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 ctr, uint32_t k0, uint32_t k1) {
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, ctr.x), lo0 = 0xD2511F53u * ctr.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, ctr.z), lo1 = 0xCD9E8D57u * ctr.z;
+    ctr = make_uint4(hi1 ^ ctr.y ^ k0, lo1, hi0 ^ ctr.w ^ k1, lo0);
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return ctr;
+}
+
+__device__ __forceinline__ void store4(void* out, int dtype, int64_t i, const float* f) {
+  if (dtype == MSDA_F32) {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + i) = make_float4(f[0], f[1], f[2], f[3]);
+  } else if (dtype == MSDA_F16) {
+    const __half2 a = __halves2half2(__float2half_rn(f[0]), __float2half_rn(f[1]));
+    const __half2 b = __halves2half2(__float2half_rn(f[2]), __float2half_rn(f[3]));
+    *reinterpret_cast<uint2*>(reinterpret_cast<__half*>(out) + i) =
+        make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+  } else {
+    const __nv_bfloat162 a = __halves2bfloat162(__float2bfloat16_rn(f[0]), __float2bfloat16_rn(f[1]));
+    const __nv_bfloat162 b = __halves2bfloat162(__float2bfloat16_rn(f[2]), __float2bfloat16_rn(f[3]));
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + i) =
+        make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+  }
+}
+
+// CTA = 64 cells of one (camera, level) grid.  Threads 0..63 run the depth
+// contest for one cell each; then every thread owns a fixed 4-channel chunk
+// (C % 4 == 0) and walks the cells with stride blockDim / (C / 4).
+__global__ void __launch_bounds__(256) paint_kernel(PaintArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Rect* s_r = reinterpret_cast<Rect*>(smem_raw);
+  __shared__ int s_win[kPaintCells];
+  const int t = blockIdx.y;  // tile = cam * L + level
+  const int cam = t / a.L, level = t - cam * a.L;
+  const int H = a.shape[2 * t], W = a.shape[2 * t + 1];
+  const int cell0 = blockIdx.x * kPaintCells;
+  if (cell0 >= H * W) return;
+  for (int e = threadIdx.x; e < a.n_ent; e += blockDim.x) s_r[e] = a.rects[(int64_t)cam * a.n_ent + e];
+  __syncthreads();
+  const double stride = a.strides[level];
+  if (threadIdx.x < kPaintCells) {
+    const int cell = cell0 + threadIdx.x;
+    int win = -1;
+    if (cell < H * W) {
+      const int y = cell / W, x = cell - y * W;
+      const double u = __dmul_rn((double)x + 0.5, stride), v = __dmul_rn((double)y + 0.5, stride);
+      double best = INFINITY;
+      for (int e = 0; e < a.n_ent; ++e) {
+        const Rect r = s_r[e];
+        if (r.valid && r.u0 <= u && u <= r.u1 && r.v0 <= v && v <= r.v1 && r.depth < best) {
+          best = r.depth;
+          win = e;
+        }
+      }
+    }
+    s_win[threadIdx.x] = win < a.n_obj ? win : -1;  // occluders paint nothing
+  }
+  __syncthreads();
+  const int n_cells = min(kPaintCells, H * W - cell0);
+  const int chunks = a.C >> 2;  // 4-channel chunks per cell
+  const int c4 = threadIdx.x % chunks;
+  const int cstep = blockDim.x / chunks;
+  if ((int)threadIdx.x >= cstep * chunks) return;
+  const int64_t row0 = a.start[t] + cell0;
+  for (int cl = threadIdx.x / chunks; cl < n_cells; cl += cstep) {
+    const int64_t o = (row0 + cl) * a.C + 4 * c4;
+    double v[4];
+    if (a.bg) {
+      const double4 b = *reinterpret_cast<const double4*>(a.bg + o);  // f64 background row chunk
+      v[0] = b.x;
+      v[1] = b.y;
+      v[2] = b.z;
+      v[3] = b.w;
+    } else {  // device background: one Philox4x32-10 draw -> four N(0, sigma) (Box-Muller, f32)
+      const uint4 r = philox4x32_10(make_uint4((uint32_t)(o >> 2), (uint32_t)(o >> 34), (uint32_t)t,
+                                               (uint32_t)a.frame), a.key0, a.key1);
+      // 23-bit uniforms via the exponent trick: (0, 1] for the logs, [0, 1) for the angles
+      const float u1 = 2.0f - __uint_as_float((r.x >> 9) | 0x3f800000u);
+      const float u3 = 2.0f - __uint_as_float((r.z >> 9) | 0x3f800000u);
+      const float a1 = __uint_as_float((r.y >> 9) | 0x3f800000u) - 1.0f;
+      const float a2 = __uint_as_float((r.w >> 9) | 0x3f800000u) - 1.0f;
+      const float m1 = sqrtf(-2.0f * __logf(u1)) * a.sigma, m2 = sqrtf(-2.0f * __logf(u3)) * a.sigma;
+      float s1, c1, s2, c2;
+      __sincosf(6.283185307f * a1, &s1, &c1);
+      __sincosf(6.283185307f * a2, &s2, &c2);
+      const int w = s_win[cl];
+      if (w < 0) {  // background only: straight to the storage dtype
+        const float nz[4] = {m1 * c1, m1 * s1, m2 * c2, m2 * s2};
+        store4(a.out, a.dtype, o, nz);
+        continue;
+      }
+      v[0] = m1 * c1;
+      v[1] = m1 * s1;
+      v[2] = m2 * c2;
+      v[3] = m2 * s2;
+    }
+    const int w = s_win[cl];
+    if (w >= 0) {  // simulator.py:288 values[mask] += signature (f64)
+      const double4 sg = *reinterpret_cast<const double4*>(a.sig + (int64_t)w * a.C + 4 * c4);
+      v[0] = __dadd_rn(v[0], sg.x);
+      v[1] = __dadd_rn(v[1], sg.y);
+      v[2] = __dadd_rn(v[2], sg.z);
+      v[3] = __dadd_rn(v[3], sg.w);
+    }
+    float f[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) f[j] = __double2float_rn(v[j]);  // simulator.py:289 astype(np.float32)
+    store4(a.out, a.dtype, o, f);
+  }
+}
+
 }  // namespace
 }  // namespace msda
 
@@ -168,6 +310,52 @@ int32_t msda_visibility(const msda_cameras_t* cams, const int32_t* image_wh, int
       cudaFuncSetAttribute(visible_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return MSDA_CUDA_ERROR;
   visible_kernel<<<dim3((unsigned)n_objects, (unsigned)n_cams), 256, smem, s>>>(a);
+  return cudaGetLastError() == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
+}
+
+size_t msda_paint_workspace_size(int32_t n_cams, int32_t n_entities) {
+  return align_up((size_t)n_cams * n_entities * sizeof(Rect), 256);
+}
+
+int32_t msda_paint(const msda_cameras_t* cams, int32_t n_cams, int32_t n_levels, const double* strides,
+                   const int32_t* spatial_shape, const int32_t* spatial_shape_host, const int64_t* scale_start_index,
+                   int32_t channels, const double* entities, int32_t n_objects, int32_t n_occluders,
+                   const double* signatures, const double* background, float sigma, uint64_t seed, int32_t frame,
+                   int32_t out_dtype, void* out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!cams || !cams->K || !cams->R || !cams->t || n_cams <= 0 || n_levels <= 0 || channels <= 0) return MSDA_BAD_ARG;
+  if (!strides || !spatial_shape || !spatial_shape_host || !scale_start_index || !out) return MSDA_BAD_ARG;
+  if (n_objects < 0 || n_occluders < 0 || out_dtype < MSDA_F32 || out_dtype > MSDA_BF16) return MSDA_BAD_ARG;
+  const int32_t n_ent = n_objects + n_occluders;
+  if (n_ent > 0 && (!entities || !workspace || workspace_bytes < msda_paint_workspace_size(n_cams, n_ent)))
+    return MSDA_BAD_ARG;
+  if (n_objects > 0 && !signatures) return MSDA_BAD_ARG;
+  if (channels % 4 || channels / 4 > 256) return MSDA_BAD_ARG;  // 4-channel chunks, one pass of a CTA per cell
+  // vector access: 4 channels per thread (double4 reads, 16/8-B writes)
+  if (reinterpret_cast<uintptr_t>(out) % 16 || reinterpret_cast<uintptr_t>(background) % 32 ||
+      reinterpret_cast<uintptr_t>(signatures) % 32)
+    return MSDA_BAD_ARG;
+  const size_t smem = (size_t)n_ent * sizeof(Rect);
+  if (smem > 200 * 1024) return MSDA_BAD_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Rect* rects = reinterpret_cast<Rect*>(workspace);
+  if (n_ent > 0) {
+    VisArgs va{cams->K, cams->R, cams->t, nullptr, entities, n_cams, n_ent, 2, rects, nullptr, nullptr};
+    const int64_t pairs = (int64_t)n_cams * n_ent;
+    rect_kernel<<<(unsigned)((pairs + 127) / 128), 128, 0, s>>>(va);
+    if (cudaGetLastError() != cudaSuccess) return MSDA_CUDA_ERROR;
+  }
+  int max_cells = 0;
+  for (int i = 0; i < n_cams * n_levels; ++i) {
+    if (spatial_shape_host[2 * i] <= 0 || spatial_shape_host[2 * i + 1] <= 0) return MSDA_BAD_ARG;
+    max_cells = std::max(max_cells, spatial_shape_host[2 * i] * spatial_shape_host[2 * i + 1]);
+  }
+  PaintArgs a{rects, strides, spatial_shape, scale_start_index, signatures, background, out, n_cams, n_levels,
+              channels, n_ent, n_objects, out_dtype, frame, sigma, (uint32_t)seed, (uint32_t)(seed >> 32)};
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(paint_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return MSDA_CUDA_ERROR;
+  const dim3 grid((unsigned)((max_cells + kPaintCells - 1) / kPaintCells), (unsigned)(n_cams * n_levels));
+  paint_kernel<<<grid, 256, smem, s>>>(a);
   return cudaGetLastError() == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
 }
 

@@ -19,6 +19,7 @@ from __future__ import annotations
 import ctypes
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from . import _lib as L
@@ -322,3 +323,115 @@ def visibility(cameras: Cameras, image_wh, objects, grid: int = 64):
     if code != L.MSDA_OK:
         raise_for_status(code, -1, "visibility")
     return vis, behind.bool()
+
+
+class PaintScene:
+    """A scene prepared for feature painting (simulator.py:249-289): cameras,
+    level grids (ceil(image / stride), simulator.py:252-253), the table
+    layout, entity boxes and signatures resident on device.  ``run`` paints
+    one frame into the channel-last table the MSDA path reads.
+
+    ``entities`` [n_objects + n_occluders, 7] f64 (x, y, z, w, l, h, yaw):
+    moving objects first (``signatures`` [n_objects, C] f64), then occluders.
+    """
+
+    def __init__(self, cameras: Cameras, image_wh, strides, channels, entities, n_objects, signatures=None):
+        import math
+
+        dev = cameras.K.device
+        wh = np.asarray(image_wh, dtype=np.int64).reshape(-1, 2)
+        n_cams = int(cameras.K.shape[0])
+        if wh.shape[0] != n_cams:
+            raise ValueError("one image size per camera")
+        if channels <= 0 or channels % 4:
+            raise ValueError("channels must be a positive multiple of 4")
+        st = [float(x) for x in np.asarray(strides, dtype=np.float64).reshape(-1)]
+        n_levels = len(st)
+        shape = np.array([[[int(math.ceil(h / s)), int(math.ceil(w / s))] for s in st] for w, h in wh],
+                         dtype=np.int32)
+        start = np.zeros((n_cams, n_levels), dtype=np.int64)
+        rows = 0
+        for c in range(n_cams):
+            for m in range(n_levels):
+                start[c, m] = rows
+                rows += int(shape[c, m, 0] * shape[c, m, 1])
+        self.ent = torch.as_tensor(np.asarray(entities, dtype=np.float64).reshape(-1, 7)).to(dev).contiguous()
+        n_ent = int(self.ent.shape[0])
+        if not 0 <= n_objects <= n_ent:
+            raise ValueError("n_objects must be within the entity count")
+        self.sig = None
+        if n_objects:
+            self.sig = torch.as_tensor(np.asarray(signatures, dtype=np.float64)).to(dev).contiguous()
+            if tuple(self.sig.shape) != (n_objects, channels):
+                raise ValueError("signatures must be [n_objects, channels]")
+        self.cameras, self.device = cameras, dev
+        self.n_cams, self.n_levels, self.channels, self.rows = n_cams, n_levels, int(channels), rows
+        self.n_objects, self.n_ent = int(n_objects), n_ent
+        self.shape_host = torch.from_numpy(np.ascontiguousarray(shape))
+        self.start_host = torch.from_numpy(start)
+        self.d_shape = self.shape_host.to(dev)
+        self.d_start = self.start_host.to(dev)
+        self.d_strides = torch.tensor(st, dtype=torch.float64, device=dev)
+        self.ws = torch.empty(max(256, int(L.lib().msda_paint_workspace_size(n_cams, n_ent))), dtype=torch.uint8,
+                              device=dev)
+
+    def run(self, background=None, sigma=0.01, seed=0, frame=0, dtype=torch.float32, out=None):
+        """Paint one frame.  ``background``: f64 [rows, C] (the reference's
+        numpy draw gives a bit-identical table) or None for a device Philox
+        N(0, sigma) draw keyed by (seed, frame).  Returns ``DeviceFeatures``."""
+        bg = None
+        if background is not None:
+            bg = torch.as_tensor(background, dtype=torch.float64).to(self.device).contiguous()
+            if tuple(bg.shape) != (self.rows, self.channels):
+                raise ValueError(f"background must be [{self.rows}, {self.channels}]")
+        if out is None:
+            out = torch.empty((self.rows, self.channels), dtype=dtype, device=self.device)
+        elif tuple(out.shape) != (self.rows, self.channels) or not out.is_contiguous():
+            raise ValueError("out must be a contiguous [rows, C] tensor")
+        cd = self.cameras.descriptor()
+        code = L.lib().msda_paint(ctypes.byref(cd), self.n_cams, self.n_levels, _ptr(self.d_strides),
+                                  _ptr(self.d_shape), _ptr(self.shape_host), _ptr(self.d_start), self.channels,
+                                  _ptr(self.ent), self.n_objects, self.n_ent - self.n_objects, _ptr(self.sig),
+                                  _ptr(bg), float(sigma), int(seed) & 0xFFFFFFFFFFFFFFFF, int(frame),
+                                  _DTYPES[out.dtype], _ptr(out), _ptr(self.ws), self.ws.numel(),
+                                  _stream(self.device))
+        if code != L.MSDA_OK:
+            raise_for_status(code, -1, "paint")
+        return DeviceFeatures(out, self.shape_host, self.start_host)
+
+
+def paint(cameras: Cameras, image_wh, strides, channels, entities, n_objects, signatures=None, background=None,
+          sigma=0.01, seed=0, frame=0, dtype=torch.float32):
+    """One-shot ``PaintScene(...).run(...)``: the painted channel-last table
+    (``DeviceFeatures``) of every camera's pyramid."""
+    return PaintScene(cameras, image_wh, strides, channels, entities, n_objects, signatures).run(
+        background, sigma, seed, frame, dtype)
+
+
+def association_cost(q_centers, d_centers, q_embeddings, d_embeddings, gate_radius=2.0, alpha_emb=1.0,
+                     alpha_geo=1.0, device=None):
+    """The tracker's association cost matrices (tracker.py:119-128) on device,
+    f64 and bit-identical to the reference's numpy.
+
+    Returns (cost, solver_cost, admissible) [n_q, n_d]."""
+    if device is None:
+        device = q_embeddings.device if torch.is_tensor(q_embeddings) else torch.device("cuda")
+    t = lambda a, n: torch.as_tensor(a, dtype=torch.float64).to(device).reshape(-1, n).contiguous()  # noqa: E731
+    qe = torch.as_tensor(q_embeddings, dtype=torch.float64).to(device).contiguous()
+    de = torch.as_tensor(d_embeddings, dtype=torch.float64).to(device).contiguous()
+    if qe.dim() != 2 or de.dim() != 2 or qe.shape[1] != de.shape[1]:
+        raise ValueError("embeddings must be [n, D] with one D")
+    n_q, n_d, dim = int(qe.shape[0]), int(de.shape[0]), int(qe.shape[1])
+    qc, dc = t(q_centers, 3), t(d_centers, 3)
+    if qc.shape[0] != n_q or dc.shape[0] != n_d:
+        raise ValueError("one centre per query / detection")
+    cost = torch.empty((n_q, n_d), dtype=torch.float64, device=device)
+    solver = torch.empty_like(cost)
+    adm = torch.empty((n_q, n_d), dtype=torch.uint8, device=device)
+    code = L.lib().msda_assoc_cost(_ptr(qc), _ptr(dc), _ptr(qe), _ptr(de), n_q, n_d, dim, float(gate_radius),
+                                   float(alpha_emb), float(alpha_geo), _ptr(cost), _ptr(solver), _ptr(adm),
+                                   _stream(device))
+    if code != L.MSDA_OK:
+        raise_for_status(code, -1, "association_cost")
+    return cost, solver, adm.bool()
+

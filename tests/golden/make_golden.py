@@ -279,8 +279,103 @@ def visibility_case():
     return out
 
 
+def paint_case():
+    """paint_pyramids (simulator.py:249-315) on three scenes: several cameras,
+    walkers, occluders, a nearer-object-wins overlap; frame 1 of each."""
+    from mvtrack3d.simulator import FeatureParams, SceneConfig, SceneObject, paint_pyramids, simulate_truth
+
+    out = {}
+    specs = [
+        # (seed, cameras [(pos, target, focal, (W, H))], walkers [(id, waypoints, dims)], occluders, C, strides)
+        (3, [([0.0, -8.0, 3.0], [0.0, 0.0, 1.0], 200.0, (320, 240)), ([8.0, 0.0, 3.0], [0.0, 0.0, 1.0], 180.0, (300, 200))],
+         [(0, [[0.0, -2.0, 0.0, 0.875], [4.0, 2.0, 0.0, 0.875]], (0.6, 0.6, 1.75)),
+          (5, [[0.0, 0.0, 1.0, 0.9], [4.0, 1.0, -2.0, 0.9]], (0.8, 0.7, 1.8))],
+         [[0.0, -4.0, 1.25, 0.3, 3.0, 2.5, 0.0]], 8, (8.0, 16.0)),
+        (11, [([0.0, -9.0, 4.0], [0.0, 0.0, 1.0], 250.0, (352, 128)), ([-6.0, -6.0, 3.0], [0.0, 0.0, 0.9], 220.0, (352, 128)),
+              ([6.0, 6.0, 3.5], [0.0, 0.0, 0.9], 240.0, (352, 128))],
+         [(1, [[0.0, 0.0, -4.0, 1.0]], (1.0, 1.0, 1.8)), (2, [[0.0, 0.0, 0.0, 1.0]], (3.0, 3.0, 2.4)),
+          (7, [[0.0, 2.0, 1.0, 0.9], [5.0, -1.0, 1.0, 0.9]], (0.5, 0.5, 1.7))],
+         [[1.5, -3.0, 1.0, 0.4, 2.0, 2.0, 0.3], [-2.0, 1.0, 1.0, 1.0, 1.0, 2.0, 1.1]], 16, (4.0, 8.0, 16.0, 32.0)),
+        (29, [([0.0, -5.0, 2.0], [0.0, 0.0, 1.0], 450.0, (640, 360))],
+         [(3, [[0.0, -1.0, 0.0, 0.9]], (0.6, 0.6, 1.75)), (4, [[0.0, 1.0, 0.5, 0.9]], (0.7, 0.6, 1.8))],
+         [], 4, (16.0, 32.0)),
+    ]
+    for k, (seed, cams, walkers, occ, C, strides) in enumerate(specs):
+        cameras = {ci: G.camera_looking_at(pos, tgt, f, (wh[0] / 2.0, wh[1] / 2.0), wh)
+                   for ci, (pos, tgt, f, wh) in enumerate(cams)}
+        objs = [SceneObject(category="person", identity=i, dims=d, waypoints=np.array(wp)) for i, wp, d in walkers]
+        cfg = SceneConfig(seed=seed, frame_rate=10.0, duration=0.1, cameras=cameras, objects=objs,
+                          occluders=[G.ObjectState3D(*o) for o in occ],
+                          features=FeatureParams(channels=C, strides=strides, background_sigma=0.01), visibility_grid=8)
+        ft = simulate_truth(cfg)[1]
+        pyr = paint_pyramids(cfg, ft)
+        ents = [[t.state.x, t.state.y, t.state.z, t.state.w, t.state.l, t.state.h, t.state.yaw] for t in ft.objects]
+        ents += [list(o) for o in occ]
+        out[f"seed{k}"] = np.array([seed, ft.frame_index, C], dtype=np.int64)
+        out[f"ids{k}"] = np.array([t.identity for t in ft.objects], dtype=np.int64)
+        out[f"n_occ{k}"] = np.array(len(occ))
+        out[f"ent{k}"] = np.array(ents, dtype=float)
+        out[f"strides{k}"] = np.array(strides, dtype=float)
+        c_ids = sorted(cameras)
+        out[f"K{k}"] = np.array([[cameras[c].focal_x, cameras[c].focal_y, cameras[c].principal_x,
+                                  cameras[c].principal_y] for c in c_ids])
+        out[f"R{k}"] = np.array([cameras[c].rotation for c in c_ids])
+        out[f"t{k}"] = np.array([cameras[c].translation for c in c_ids])
+        out[f"wh{k}"] = np.array([[cameras[c].width, cameras[c].height] for c in c_ids], dtype=np.int32)
+        out[f"table{k}"] = np.concatenate([g.values.reshape(-1, C) for c in c_ids for g in pyr[c].levels])
+    return out
+
+
+def assoc_case():
+    """The association cost of tracker.associate (tracker.py:105-142): the
+    solver_cost matrix handed to linear_sum_assignment is captured, plus the
+    resulting Assignment."""
+    from mvtrack3d import tracker as T
+    from mvtrack3d.oae import Embedding, Query
+
+    captured = []
+    real = T.linear_sum_assignment
+
+    def capture(m):
+        captured.append(np.array(m, copy=True))
+        return real(m)
+
+    T.linear_sum_assignment = capture
+    out = {}
+    rng = np.random.default_rng(61)
+    try:
+        for k, (n_q, n_d, D, gate) in enumerate([(7, 9, 16, 2.0), (30, 25, 128, 1.5), (12, 12, 128, float("inf")),
+                                                 (40, 33, 64, 3.0)]):
+            def unit(n):
+                v = rng.standard_normal((n, D))
+                return v / np.linalg.norm(v, axis=1, keepdims=True)
+
+            qe, de = unit(n_q), unit(n_d)
+            qc = rng.uniform(-5, 5, (n_q, 3))
+            dc = np.concatenate([qc[: n_d // 2] + rng.normal(0, 0.5, (n_d // 2, 3)),
+                                 rng.uniform(-5, 5, (n_d - n_d // 2, 3))])
+            ids = rng.permutation(1000)[:n_q]
+            queries = [Query(track_id=int(ids[i]), anchor=G.ObjectState3D(*qc[i], 0.6, 0.6, 1.7, 0.0),
+                             memory=Embedding(qe[i]), descriptor=np.zeros(D)) for i in range(n_q)]
+            dets = [T.Detection(state=G.ObjectState3D(*dc[j], 0.6, 0.6, 1.7, 0.0), embedding=Embedding(de[j]),
+                                confidence=1.0) for j in range(n_d)]
+            params = T.TrackerParams(gate_radius=gate, alpha_emb=0.7 + 0.1 * k, alpha_geo=1.3 - 0.2 * k)
+            asg = T.associate(T.QueryBank(queries=queries), dets, params)
+            order = np.argsort(ids, kind="stable")  # the reference sorts queries by track id
+            out[f"qc{k}"], out[f"dc{k}"] = qc[order], dc
+            out[f"qe{k}"], out[f"de{k}"] = qe[order], de
+            out[f"par{k}"] = np.array([gate, params.alpha_emb, params.alpha_geo])
+            out[f"solver{k}"] = captured[-1]
+            out[f"matches{k}"] = np.array(asg.matches, dtype=np.int64).reshape(-1, 2)
+            out[f"total{k}"] = np.array(asg.total_cost)
+            out[f"qids{k}"] = ids[order]
+    finally:
+        T.linear_sum_assignment = real
+    return out
+
+
 def main():
-    jobs = [("visibility", visibility_case), ("fpyr", fpyr_case), ("crit1", crit1), ("features", features_cases), ("bench", bench_cases), ("dense", dense_cases),
+    jobs = [("paint", paint_case), ("assoc", assoc_case), ("visibility", visibility_case), ("fpyr", fpyr_case), ("crit1", crit1), ("features", features_cases), ("bench", bench_cases), ("dense", dense_cases),
             ("projection", projection_cases), ("oae", oae_cases)]
     only = set(sys.argv[1:])
     for name, fn in jobs:

@@ -180,6 +180,45 @@ def oae_case(reps, dev, cams=32, C=256, Q=900):
             "queries_per_s": Q / (med / 1e3)}
 
 
+def paint_case(reps, dev, cams=64, C=256, n_obj=40, n_occ=8):
+    """Feature painting of a cfg3-shaped scene (64 ring cameras, 704x256
+    images, strides 4-32, C=256) straight into the f16 table, device
+    background: HBM-write bound (the table is the algorithmic byte count)."""
+    K, R, T = ring(cams)
+    camd = ops.Cameras(K, R, T, device=dev)
+    rng = torch.Generator().manual_seed(9)
+    ents = torch.cat([torch.rand((n_obj + n_occ, 2), generator=rng) * 8 - 4, torch.full((n_obj + n_occ, 1), 0.9),
+                      torch.tensor([[0.6, 0.6, 1.8]]).repeat(n_obj + n_occ, 1),
+                      torch.rand((n_obj + n_occ, 1), generator=rng) * 6.28 - 3.14], dim=1).double().numpy()
+    sig = torch.nn.functional.normalize(torch.randn((n_obj, C), generator=rng, dtype=torch.float64), dim=1).numpy()
+    wh = [[704, 256]] * cams
+    strides = [4.0, 8.0, 16.0, 32.0]
+    scene = ops.PaintScene(camd, wh, strides, C, ents, n_obj, sig)
+    out = torch.empty((scene.rows, C), dtype=torch.float16, device=dev)
+    fn = lambda: scene.run(sigma=0.01, seed=1, out=out)  # noqa: E731
+    nbytes = out.numel() * 2
+    med, best = time_fn(fn, reps, flush=False)
+    gbs = nbytes / (med / 1e3) / 1e9
+    return {"config": "paint-cfg3", "path": "paint (depth contest + signature + device N(0, sigma), f16 table)",
+            "dtype": "float16", "cams": cams, "entities": n_obj + n_occ, "latency_us": med * 1e3,
+            "best_us": best * 1e3, "table_bytes": nbytes, "achieved_gbs": gbs, "frac": gbs / peak()}
+
+
+def assoc_case(reps, dev, n_q=900, n_d=900, D=256):
+    """Association cost matrices for a 900-query bank vs 900 detections, D=256
+    (the OAE embedding dimension at C=256), f64."""
+    g = torch.Generator(device=dev).manual_seed(12)
+    qc = torch.rand((n_q, 3), generator=g, device=dev, dtype=torch.float64) * 10 - 5
+    dc = torch.rand((n_d, 3), generator=g, device=dev, dtype=torch.float64) * 10 - 5
+    qe = torch.nn.functional.normalize(torch.randn((n_q, D), generator=g, device=dev, dtype=torch.float64), dim=1)
+    de = torch.nn.functional.normalize(torch.randn((n_d, D), generator=g, device=dev, dtype=torch.float64), dim=1)
+    fn = lambda: ops.association_cost(qc, dc, qe, de, 2.0, 1.0, 1.0, device=dev)  # noqa: E731
+    med, best = time_fn(fn, reps, flush=False)
+    return {"config": "assoc-900x900", "path": "association_cost (f64, numpy pairwise order)", "dtype": "float64",
+            "n_q": n_q, "n_d": n_d, "dim": D, "latency_us": med * 1e3, "best_us": best * 1e3,
+            "pairs_per_s": n_q * n_d / (med / 1e3)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
@@ -197,9 +236,13 @@ def main():
                                    torch.float16, "fast", args.reps, dev),
         "cfg3_h2": lambda: dense_case("cfg3 64 cams fp16, half2 accumulation", 64, CFG1_LEVELS, 256, 8,
                                       torch.float16, "fast_h2", args.reps, dev),
+        "cfg4d": lambda: dense_case("cfg4 MSDA part: 32 cams bf16", 32, CFG1_LEVELS, 256, 8, torch.bfloat16, "fast",
+                                    args.reps, dev),
         "cfg5": lambda: dense_case("cfg5 512 cams fp16 (1 GPU)", 512, CFG1_LEVELS, 256, 8, torch.float16, "fast",
                                    max(5, args.reps // 4), dev),
         "project": lambda: project_case(args.reps, dev),
+        "paint": lambda: paint_case(args.reps, dev),
+        "assoc": lambda: assoc_case(args.reps, dev),
         "cfg4": lambda: oae_case(max(5, args.reps // 4), dev),
     }
     for name, fn in cases.items():
