@@ -141,12 +141,19 @@ __device__ void canon_slots(int n, int n_tiles, u64* kt, u64* kp, int32_t* sdst,
       const uint32_t t = (uint32_t)(it >> 32);
       const int rs = s_run[2 * t], re = s_run[2 * t + 1];
       int rank = 0;
-      for (int j = rs; j < re; ++j) {
+      bool tie = false;
+#pragma unroll 4
+      for (int j = rs; j < re; ++j) {  // branch-free: one 64-bit (v, u) compare per run member
         const u64 jp = kp[j];
         rank += jp < ip ? 1 : 0;
-        if (jp == ip) {  // exact (v, u) tie: weight, then position
-          const uint32_t wj = (uint32_t)kt[j], wi = (uint32_t)it;
-          rank += (j != i && (wj < wi || (wj == wi && j < i))) ? 1 : 0;
+        tie |= (jp == ip) & (j != i);
+      }
+      if (tie) {  // exact (v, u) tie (rare): weight, then position
+        const uint32_t wi = (uint32_t)it;
+        for (int j = rs; j < re; ++j) {
+          if (j == i || kp[j] != ip) continue;
+          const uint32_t wj = (uint32_t)kt[j];
+          rank += (wj < wi || (wj == wi && j < i)) ? 1 : 0;
         }
       }
       sdst[i] = rs + rank;
@@ -215,21 +222,42 @@ template <bool SMEM>
 __device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_t lo, int n, int n_tiles, u64* khi,
                                             u64* klo, float* sw, int32_t* sdst, int16_t* s_run, float* s_wsum) {
   {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const int64_t s = lo + i;
-      int c = a.cam[s], l = a.lvl[s];
-      const float uu = a.u[s], vv = a.v[s], ww = a.w[s];
-      if (c < 0 || c >= a.n_cams || l < 0 || l >= a.n_levels) {
-        set_status(a.status, MSDA_BAD_TARGET, s);
-        c = 0;
-        l = 0;
+    constexpr int U = 4;  // samples per thread whose loads are in flight together
+    for (int i0 = threadIdx.x; i0 < n; i0 += U * blockDim.x) {
+      int c[U], l[U];
+      float uu[U], vv[U], ww[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int i = i0 + j * (int)blockDim.x;
+        if (i < n) {
+          const int64_t s = lo + i;
+          c[j] = __ldg(a.cam + s);
+          l[j] = __ldg(a.lvl + s);
+          uu[j] = __ldg(a.u + s);
+          vv[j] = __ldg(a.v + s);
+          ww[j] = __ldg(a.w + s);
+        }
       }
-      if (!(isfinite(uu) && isfinite(vv) && isfinite(ww))) set_status(a.status, MSDA_NONFINITE, s);
-      khi[i] = ((u64)(c * a.n_levels + l) << 32) | ord_f32(ww);  // kt: tile, weight
-      klo[i] = ((u64)ord_f32(vv) << 32) | ord_f32(uu);            // kp: v, u
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const int i = i0 + j * (int)blockDim.x;
+        if (i < n) {
+          if (c[j] < 0 || c[j] >= a.n_cams || l[j] < 0 || l[j] >= a.n_levels) {
+            set_status(a.status, MSDA_BAD_TARGET, lo + i);
+            c[j] = 0;
+            l[j] = 0;
+          }
+          if (!(isfinite(uu[j]) && isfinite(vv[j]) && isfinite(ww[j]))) set_status(a.status, MSDA_NONFINITE, lo + i);
+          khi[i] = ((u64)(c[j] * a.n_levels + l[j]) << 32) | ord_f32(ww[j]);  // kt: tile, weight
+          klo[i] = ((u64)ord_f32(vv[j]) << 32) | ord_f32(uu[j]);               // kp: v, u
+        }
+      }
     }
     __syncthreads();
     canon_slots(n, n_tiles, khi, klo, sdst, sw, s_run);
+    // thread 0 runs the sequential f32 weight sum (features.py:264-269) while
+    // the other threads write the records, which do not depend on it
+    const int64_t row_base = (q / a.queries_per_batch) * a.rows_per_batch;
     if (threadIdx.x == 0) {
       float ws = 0.0f;
       if (a.normalize) {
@@ -237,21 +265,20 @@ __device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_
         if (ws == 0.0f) set_status(a.status, MSDA_ZERO_WEIGHT_SUM, q);
       }
       *s_wsum = ws;
+    } else {
+      for (int i = threadIdx.x - 1; i < n; i += blockDim.x - 1) {
+        const u64 kt = khi[i], kp = klo[i];
+        const int t = (int)(kt >> 32);
+        const float vv = unord_f32((uint32_t)(kp >> 32));
+        const float uu = unord_f32((uint32_t)(kp & 0xffffffffu));
+        const int tt = t < n_tiles ? t : 0;
+        a.rec[lo + sdst[i]] = make_record(uu, vv, row_base + a.start[tt], a.shape[2 * tt], a.shape[2 * tt + 1]);
+      }
     }
     __syncthreads();
     const float wsum = *s_wsum;
-    const int64_t row_base = (q / a.queries_per_batch) * a.rows_per_batch;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const u64 kt = khi[i], kp = klo[i];
-      const int dst = sdst[i];
-      const int t = (int)(kt >> 32);
-      const float vv = unord_f32((uint32_t)(kp >> 32));
-      const float uu = unord_f32((uint32_t)(kp & 0xffffffffu));
-      const float ww = key_weight(kt);
-      const int tt = t < n_tiles ? t : 0;
-      a.rec[lo + dst] = make_record(uu, vv, row_base + a.start[tt], a.shape[2 * tt], a.shape[2 * tt + 1]);
-      a.wn[lo + dst] = a.normalize ? __fdiv_rn(ww, wsum) : ww;
-    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x)  // canonical slot order: coalesced
+      a.wn[lo + i] = a.normalize ? __fdiv_rn(sw[i], wsum) : sw[i];
     __syncthreads();
   }
 }
