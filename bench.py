@@ -141,13 +141,30 @@ def algorithmic_bytes(gw):
             x, y = x0 + dx, y0 + dy
             ok = (x >= 0) & (x < W) & (y >= 0) & (y < H)
             rows.append((gw.tile_start[t] + y * W + x)[ok])
+    gathered = int(sum(r.size for r in rows))  # in-grid corner rows the gather moves (L2 -> SM)
     touched = np.unique(np.concatenate(rows)).size
     s_n, q_n = gw.us.size, wl.queries
     feat_b = touched * wl.channels * 4
     in_b = s_n * 20 + (q_n + 1) * 8
     out_b = q_n * wl.channels * 4 + q_n
     return {"touched_cells": int(touched), "touched_frac": touched / gw.table.shape[0], "feature_bytes": feat_b,
-            "input_bytes": in_b, "output_bytes": out_b, "total": feat_b + in_b + out_b}
+            "input_bytes": in_b, "output_bytes": out_b, "total": feat_b + in_b + out_b,
+            "gathered_corner_bytes": gathered * wl.channels * 4}
+
+
+def l2_gather_ceiling():
+    """The measured L2 -> SM random-row gather ceiling of this part (no-math
+    cp.async ring over the same rows, tools/gather_ceiling.cu), from the
+    committed profile; None when absent."""
+    p = ROOT / "profiles" / "r1" / "gather_ceiling.txt"
+    if not p.exists():
+        return None
+    best = None
+    for line in p.read_text().splitlines():
+        if line.startswith("pipe_") and "moved" in line:
+            v = float(line.split("moved")[1].split("GB/s")[0])
+            best = v if best is None else max(best, v)
+    return best
 
 
 def cpu_reference_time(gw, budget_s=15.0, reps=3, workers=None):
@@ -355,7 +372,17 @@ def run_ours(args, cfg, rank, local_rank, world):
         "roofline": {"bound": "hbm", "kernel": "gather_pipe_kernel<float,4> (exact gather)", "achieved": achieved,
                      "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": ncu_traffic(args.config),
-                     "peak_source": peak_src, "algorithmic_bytes": ab},
+                     "peak_source": peak_src, "algorithmic_bytes": ab,
+                     "secondary": {
+                         "bound": "l2_gather",
+                         "note": "the corner gathers (4 rows per sample, in-grid) cross L2 -> SM; DRAM sees each "
+                                 "touched row about once",
+                         "bytes": ab["gathered_corner_bytes"],
+                         "achieved": ab["gathered_corner_bytes"] / (g_ms / 1e3) / 1e9,
+                         "ceiling": l2_gather_ceiling(),
+                         "ceiling_source": "measured: tools/gather_ceiling.cu no-math cp.async ring on the same rows "
+                                           "(profiles/r1/gather_ceiling.txt)",
+                         "unit": "GB/s"}},
         "e2e": {"value": world * wl.cameras / e2e_s, "unit": "camera-frames/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
                 "api": "paper_2601_10819_b200.features.msda_optimized -> C-ABI msda_csr_host (pinned host buffers)",
