@@ -174,19 +174,24 @@ __global__ void oae_pool_kernel(OaeArgs a) {
 // Production shape (C == 32 * VEC): one CTA of kOaeWarps warps per query, warp
 // w takes cameras w, w + kOaeWarps, ...; a whole warp covers the channel row.
 // Per valid keypoint the 4 levels x 4 corner rows are loaded together, the
-// level mean and the descriptor score (warp all-reduce) follow, and the
-// keypoint softmax is accumulated online (running max / sum in f64, weighted
-// vector in f32), so no keypoint features are staged.  Per-warp camera partials are
+// level mean (FFMA2, the 1/L folded into the bilinear weights) and the
+// descriptor score (per-lane FFMA2, f64 warp all-reduce) follow, and the
+// keypoint softmax is accumulated online in f32 (running max / sum, weighted
+// vector), so no keypoint features are staged.  Tolerance parity: fused
+// products and f32 softmax vs the reference's f64 (<= 1e-4 on the unit
+// embedding, tests/test_gpu_dense.py).  Per-warp camera partials are
 // summed across warps at the end (tolerance-level reassociation of Eq. 2).
 
 constexpr int kOaeWarps = 8;
-constexpr int kOaeLevels = 4;  // levels loaded together (more are looped)
+constexpr int kOaeLevels = 4;   // levels loaded together (more are looped)
+constexpr int kOaeMaxRecs = 64;  // keypoints x levels staged per camera
 
 template <typename T, int VEC>
 __global__ void __launch_bounds__(kOaeWarps * 32, 2) oae_warp_kernel(OaeArgs a) {
   constexpr int NV = VEC * (int)sizeof(T) / 16;
   constexpr int LV = NV >= 2 ? 2 : kOaeLevels;  // levels in flight: bounded by registers
   __shared__ double s_kp[kOaeMaxPoints * 3];
+  __shared__ SampleRec s_rec[kOaeWarps][kOaeMaxRecs];  // per camera: every (keypoint, level) record
   __shared__ float s_fused[kOaeWarps][32 * VEC];
   __shared__ double s_vt[kOaeWarps];
   __shared__ double s_red[kOaeWarps];
@@ -201,13 +206,15 @@ __global__ void __launch_bounds__(kOaeWarps * 32, 2) oae_warp_kernel(OaeArgs a) 
       set_status(a.status, MSDA_OFFSET_RANGE, p);
   __syncthreads();
 
-  float d[VEC], fused[VEC];
+  float2 d2[VEC / 2];
+  float fused[VEC];
 #pragma unroll
-  for (int e = 0; e < VEC; ++e) {
-    d[e] = a.desc[(int64_t)q * a.C + c0 + e];
-    fused[e] = 0.0f;
+  for (int e = 0; e < VEC; e += 2) {
+    d2[e / 2] = make_float2(a.desc[(int64_t)q * a.C + c0 + e], a.desc[(int64_t)q * a.C + c0 + e + 1]);
+    fused[e] = fused[e + 1] = 0.0f;
   }
-  const double inv_sqrt_d = 1.0 / sqrt((double)a.C);
+  const float inv_sqrt_d = (float)(1.0 / sqrt((double)a.C));
+  const float inv_l = 1.0f / (float)a.L;  // level mean folded into the bilinear weights
   double vt = 0.0;
 
   for (int cam = warp; cam < a.cams; cam += kOaeWarps) {
@@ -216,17 +223,30 @@ __global__ void __launch_bounds__(kOaeWarps * 32, 2) oae_warp_kernel(OaeArgs a) 
                     project_f64(a.K + cam * 4, a.R + cam * 9, a.T + cam * 3, s_kp + 3 * min(lane, a.P - 1), up, vp);
     unsigned mask = __ballot_sync(0xffffffffu, ok);
     if (mask == 0u) continue;  // every keypoint behind: invalid view, zero weight (oae.py:114-115, 141-143)
-    double m = -INFINITY, z = 0.0;
-    float acc[VEC];
+    // every (keypoint, level) record of this camera, one per lane, staged in
+    // warp-private shared memory: cell = pixel / stride - 0.5 (features.py:45-47)
+    for (int s0 = 0; s0 < a.P * a.L; s0 += 32) {
+      const int s = s0 + lane;
+      const int kp = min(s, a.P * a.L - 1) / a.L, l = min(s, a.P * a.L - 1) % a.L;
+      const double u = __shfl_sync(0xffffffffu, up, kp), v = __shfl_sync(0xffffffffu, vp, kp);
+      if (s < a.P * a.L) {
+        const int t = cam * a.L + l;
+        const double st = (double)a.strides[l];
+        s_rec[warp][s] = make_record((float)(u / st - 0.5), (float)(v / st - 0.5), a.start[t], a.shape[2 * t],
+                                     a.shape[2 * t + 1]);
+      }
+    }
+    __syncwarp();
+    float m = -INFINITY, z = 0.0f;
+    float2 acc[VEC / 2];
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) acc[e] = 0.0f;
+    for (int e = 0; e < VEC / 2; ++e) acc[e] = make_float2(0.0f, 0.0f);
     while (mask) {
       const int p = __ffs(mask) - 1;
       mask &= mask - 1;
-      const double u = __shfl_sync(0xffffffffu, up, p), v = __shfl_sync(0xffffffffu, vp, p);
-      float g[VEC];
+      float2 g[VEC / 2];  // level mean of the bilinear reads, two channels per FFMA2
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) g[e] = 0.0f;
+      for (int e = 0; e < VEC / 2; ++e) g[e] = make_float2(0.0f, 0.0f);
       for (int l0 = 0; l0 < a.L; l0 += LV) {
         SampleRec r[LV];
         Row<NV> c[LV][4];
@@ -234,10 +254,7 @@ __global__ void __launch_bounds__(kOaeWarps * 32, 2) oae_warp_kernel(OaeArgs a) 
         for (int j = 0; j < LV; ++j) {
           const int l = l0 + j;
           if (l < a.L) {
-            const int t = cam * a.L + l;
-            const double st = (double)a.strides[l];
-            r[j] = make_record((float)(u / st - 0.5), (float)(v / st - 0.5), a.start[t], a.shape[2 * t],
-                               a.shape[2 * t + 1]);
+            r[j] = s_rec[warp][p * a.L + l];
           } else {
             r[j].row[0] = r[j].row[1] = r[j].row[2] = r[j].row[3] = -1;
           }
@@ -252,40 +269,41 @@ __global__ void __launch_bounds__(kOaeWarps * 32, 2) oae_warp_kernel(OaeArgs a) 
 #pragma unroll
         for (int j = 0; j < LV; ++j) {
           if (l0 + j >= a.L) break;
-          float f[4][VEC];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) raw_to_f32<T, VEC>(reinterpret_cast<const uint32_t*>(c[j][k].v), f[k]);
+          for (int k = 0; k < 4; ++k) {
+            float f[VEC];
+            raw_to_f32<T, VEC>(reinterpret_cast<const uint32_t*>(c[j][k].v), f);
+            const float cw = r[j].iw[k] * inv_l;
+            const float2 w2 = make_float2(cw, cw);
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) {  // reference f32 bilinear tree (features.py:219)
-            const float b = __fadd_rn(__fadd_rn(__fmul_rn(f[0][e], r[j].iw[0]), __fmul_rn(f[1][e], r[j].iw[1])),
-                                      __fadd_rn(__fmul_rn(f[2][e], r[j].iw[2]), __fmul_rn(f[3][e], r[j].iw[3])));
-            g[e] += b;
+            for (int e = 0; e < VEC / 2; ++e) g[e] = __ffma2_rn(make_float2(f[2 * e], f[2 * e + 1]), w2, g[e]);
           }
         }
       }
-      double dot = 0.0;
-      const float inv_l = 1.0f / (float)a.L;
+      float2 dp = make_float2(0.0f, 0.0f);
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) {
-        g[e] *= inv_l;  // level mean (oae.py:112)
-        dot += (double)g[e] * (double)d[e];
-      }
+      for (int e = 0; e < VEC / 2; ++e) dp = __ffma2_rn(g[e], d2[e], dp);
+      double dot = (double)dp.x + (double)dp.y;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-      const double s = dot * inv_sqrt_d;
-      const double m2 = fmax(m, s);
-      const double scale = exp(m - m2), w = exp(s - m2);  // online softmax (oae.py:117-122)
+      const float sc = (float)dot * inv_sqrt_d;
+      const float m2 = fmaxf(m, sc);
+      const float scale = expf(m - m2), w = expf(sc - m2);  // online softmax (oae.py:117-122)
       z = z * scale + w;
-      const float fs = (float)scale, fw = (float)w;
+      const float2 s2 = make_float2(scale, scale), w2 = make_float2(w, w);
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) acc[e] = acc[e] * fs + fw * g[e];
+      for (int e = 0; e < VEC / 2; ++e) acc[e] = __ffma2_rn(g[e], w2, __fmul2_rn(acc[e], s2));
       m = m2;
     }
+    __syncwarp();  // the next camera restages s_rec
     const double vis = (double)a.vis[(int64_t)q * a.cams + cam];
     vt += vis;
-    const float vz = (float)(vis / z);
+    const float vz = (float)(vis / (double)z);
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) fused[e] += vz * acc[e];
+    for (int e = 0; e < VEC / 2; ++e) {
+      fused[2 * e] += vz * acc[e].x;
+      fused[2 * e + 1] += vz * acc[e].y;
+    }
   }
 
 #pragma unroll
@@ -399,10 +417,11 @@ int32_t msda_oae_pool(const msda_features_t* f, int32_t n_queries, const float* 
   cudaError_t e;
   const int C = f->channels;
   const bool al16 = al % 16 == 0;
-  if (al16 && f->dtype == MSDA_F32 && C == 256) return launch_oae_warp<float, 8>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
-  if (al16 && f->dtype == MSDA_F32 && C == 128) return launch_oae_warp<float, 4>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
-  if (al16 && f->dtype == MSDA_F16 && C == 256) return launch_oae_warp<__half, 8>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
-  if (al16 && f->dtype == MSDA_BF16 && C == 256)
+  const bool recs_fit = a.P * a.L <= kOaeMaxRecs;
+  if (recs_fit && al16 && f->dtype == MSDA_F32 && C == 256) return launch_oae_warp<float, 8>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
+  if (recs_fit && al16 && f->dtype == MSDA_F32 && C == 128) return launch_oae_warp<float, 4>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
+  if (recs_fit && al16 && f->dtype == MSDA_F16 && C == 256) return launch_oae_warp<__half, 8>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
+  if (recs_fit && al16 && f->dtype == MSDA_BF16 && C == 256)
     return launch_oae_warp<__nv_bfloat16, 8>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
   switch (f->dtype) {
     case MSDA_F32:
