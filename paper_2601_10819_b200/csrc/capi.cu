@@ -99,8 +99,14 @@ int32_t msda_csr_stages(const msda_features_t* feat, const msda_csr_plan_t* plan
   ExactWorkspace w = carve_exact_workspace(workspace, plan->n_samples);
   if ((stage_mask & 1) && reset_exact_workspace(w, stream) != cudaSuccess) return MSDA_CUDA_ERROR;
   if (plan->n_queries == 0) return MSDA_OK;
-  // FAST on the CSR path runs the exact kernels: they already sit on the
-  // gather roofline for the reference plan shapes.
+  // FAST: any summation order, so no canonicalisation — one gather launch
+  // from the raw plan (stage 2; stage 1 only resets the status word)
+  if (precision >= MSDA_FAST && feat->batch == 1) {
+    if (!(stage_mask & 2)) return MSDA_OK;
+    const cudaError_t e = launch_csr_fast(*feat, *plan, normalize, w, out, empty, stream);
+    if (e == cudaSuccess) return MSDA_OK;
+    if (e != cudaErrorNotSupported) return MSDA_CUDA_ERROR;
+  }
   const int prec = precision >= MSDA_FAST ? MSDA_EXACT : precision;
   if ((stage_mask & 1) &&
       launch_plan_canon(*feat, *plan, normalize, w, num_sms_for_current_device(), stream) != cudaSuccess)

@@ -300,6 +300,16 @@ struct GatherArgs {
   uint8_t* empty;
   float2 one2;  // (1, 1)   — FFMA2 operands that make exact adds / products;
   float2 nz2;   // (-0, -0)   passed as parameters so ptxas cannot fuse them
+  // FAST (RAW): the raw plan, read directly — no canonicalisation
+  const int32_t* cam;
+  const int32_t* lvl;
+  const float* u;
+  const float* v;
+  const float* w;
+  const int32_t* shape;
+  const int64_t* start;
+  int32_t n_cams, n_levels, normalize;
+  DevStatus* status;
 };
 
 __device__ __forceinline__ SampleRec ld_rec(const SampleRec* p) {
@@ -463,7 +473,26 @@ struct PipeSmem {
 
 constexpr int kPipeWarps = 1;  // one warp per CTA: finest shared-memory granularity per SM
 
-template <typename T, int VEC, bool HALF, int D>
+// FAST: acc += (iw_k * wn) * c_k, fused, any order
+template <int VEC>
+__device__ __forceinline__ void fast_accumulate(float* acc, const float (*c)[VEC], const float4 iw, const float wn) {
+  const float cw[4] = {iw.x * wn, iw.y * wn, iw.z * wn, iw.w * wn};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 w2 = make_float2(cw[k], cw[k]);
+#pragma unroll
+    for (int e = 0; e < VEC; e += 2) {
+      const float2 r = __ffma2_rn(make_float2(c[k][e], c[k][e + 1]), w2, make_float2(acc[e], acc[e + 1]));
+      acc[e] = r.x;
+      acc[e + 1] = r.y;
+    }
+  }
+}
+
+// RAW = FAST on the CSR plan: records are built from the plan arrays in the
+// batch loader and the weight sum is a warp reduction (any order), so no
+// canonicalisation pass runs; the gather pipeline is the exact path's.
+template <typename T, int VEC, bool HALF, int D, bool RAW>
 __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs a) {
   constexpr int BYTES = VEC * (int)sizeof(T);
   using SM = PipeSmem<BYTES, D>;
@@ -488,6 +517,19 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   const char* featc = reinterpret_cast<const char*>(a.feat) + (size_t)(a.c_off + c0) * sizeof(T);
   const uint32_t row_bytes = (uint32_t)a.row_elems * (uint32_t)sizeof(T);
 
+  const bool head = c0 == lane * VEC;  // the query's first channel-slice warp reports plan errors
+  float wsum = 1.0f;
+  if constexpr (RAW) {
+    if (a.normalize) {  // per-query weight sum, any order (FAST)
+      float t = 0.0f;
+      for (int s = lane; s < n; s += 32) t += __ldg(a.w + lo + s);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      wsum = t;
+      if (n > 0 && wsum == 0.0f && head && lane == 0) set_status(a.status, MSDA_ZERO_WEIGHT_SUM, q);
+    }
+  }
+
   // record batch b: lane j holds sample 32 b + j
   int4 r_rows = make_int4(-1, -1, -1, -1);
   float4 r_iw = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -495,10 +537,26 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   auto load_batch = [&](int b) {
     const int s = b * 32 + lane;
     if (s < n) {
-      const SampleRec r = ld_rec(rec + s);
+      SampleRec r;
+      if constexpr (RAW) {
+        const int64_t si = lo + s;
+        int c = __ldg(a.cam + si), l = __ldg(a.lvl + si);
+        const float uu = __ldg(a.u + si), vv = __ldg(a.v + si), ww = __ldg(a.w + si);
+        if (c < 0 || c >= a.n_cams || l < 0 || l >= a.n_levels) {
+          if (head) set_status(a.status, MSDA_BAD_TARGET, si);
+          c = 0;
+          l = 0;
+        }
+        if (!(isfinite(uu) && isfinite(vv) && isfinite(ww)) && head) set_status(a.status, MSDA_NONFINITE, si);
+        const int t = c * a.n_levels + l;
+        r = make_record(uu, vv, a.start[t], a.shape[2 * t], a.shape[2 * t + 1]);
+        r_wn = a.normalize ? ww / wsum : ww;
+      } else {
+        r = ld_rec(rec + s);
+        r_wn = __ldg(wnp + s);
+      }
       r_rows = make_int4(r.row[0], r.row[1], r.row[2], r.row[3]);
       r_iw = make_float4(r.iw[0], r.iw[1], r.iw[2], r.iw[3]);
-      r_wn = __ldg(wnp + s);
     }
   };
   auto store_batch = [&](int buf) {
@@ -558,8 +616,13 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
         to_f32<T, VEC>(cv0[k], c0[k]);
         to_f32<T, VEC>(cv1[k], c1[k]);
       }
-      exact_accumulate<VEC>(accf, c0, iw0, wn0, a.one2, a.nz2);
-      if (two) exact_accumulate<VEC>(accf, c1, iw1, wn1, a.one2, a.nz2);
+      if constexpr (RAW) {
+        fast_accumulate<VEC>(accf, c0, iw0, wn0);
+        if (two) fast_accumulate<VEC>(accf, c1, iw1, wn1);
+      } else {
+        exact_accumulate<VEC>(accf, c0, iw0, wn0, a.one2, a.nz2);
+        if (two) exact_accumulate<VEC>(accf, c1, iw1, wn1, a.one2, a.nz2);
+      }
     } else {
       const void* p0[4] = {&cv0[0], &cv0[1], &cv0[2], &cv0[3]};
       const void* p1[4] = {&cv1[0], &cv1[1], &cv1[2], &cv1[3]};
@@ -607,13 +670,13 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   if (c0 == 0 && a.empty) a.empty[q] = (n == 0) ? 1 : 0;
 }
 
-template <typename T, int VEC, bool HALF, int D>
+template <typename T, int VEC, bool HALF, int D, bool RAW>
 cudaError_t launch_gather_pipe(const GatherArgs& g, cudaStream_t stream) {
   constexpr int BYTES = VEC * (int)sizeof(T);
   const int smem = kPipeWarps * PipeSmem<BYTES, D>::kPerWarp;
   static bool attr_set = false;  // per instantiation; idempotent
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gather_pipe_kernel<T, VEC, HALF, D>,
+    cudaError_t e = cudaFuncSetAttribute(gather_pipe_kernel<T, VEC, HALF, D, RAW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
@@ -621,16 +684,23 @@ cudaError_t launch_gather_pipe(const GatherArgs& g, cudaStream_t stream) {
   const int64_t warps = g.n_queries * (g.C / VEC / 32);
   const int64_t grid = (warps + kPipeWarps - 1) / kPipeWarps;
   if (grid == 0) return cudaSuccess;
-  gather_pipe_kernel<T, VEC, HALF, D><<<(unsigned)grid, kPipeWarps * 32, smem, stream>>>(g);
+  gather_pipe_kernel<T, VEC, HALF, D, RAW><<<(unsigned)grid, kPipeWarps * 32, smem, stream>>>(g);
   return cudaGetLastError();
 }
 
 template <typename T, int VEC, bool HALF>
-cudaError_t launch_gather(const GatherArgs& g, cudaStream_t stream) {
+cudaError_t launch_gather(const GatherArgs& g, cudaStream_t stream, bool raw) {
   if ((g.C / VEC) % 32 == 0 && g.C % VEC == 0) {
-    if constexpr (VEC * sizeof(T) == 16) return launch_gather_pipe<T, VEC, HALF, 7>(g, stream);
-    else return launch_gather_pipe<T, VEC, HALF, 12>(g, stream);
+    if constexpr (!HALF) {
+      if (raw) {
+        if constexpr (VEC * sizeof(T) == 16) return launch_gather_pipe<T, VEC, HALF, 7, true>(g, stream);
+        else return launch_gather_pipe<T, VEC, HALF, 12, true>(g, stream);
+      }
+    }
+    if constexpr (VEC * sizeof(T) == 16) return launch_gather_pipe<T, VEC, HALF, 7, false>(g, stream);
+    else return launch_gather_pipe<T, VEC, HALF, 12, false>(g, stream);
   }
+  if (raw) return cudaErrorNotSupported;
   const int lanes = g.C / VEC;
   const int64_t threads = g.n_queries * lanes;
   const int block = 256;
@@ -714,8 +784,9 @@ cudaError_t launch_plan_canon(const msda_features_t& f, const msda_csr_plan_t& p
 
 cudaError_t launch_gather_exact(const msda_features_t& f, const msda_csr_plan_t& p, int precision,
                                 const ExactWorkspace& w, float* out, uint8_t* empty, cudaStream_t stream,
-                                int c_off, int c_count) {
-  GatherArgs g;
+                                int c_off, int c_count, int fast_normalize) {
+  const bool raw = fast_normalize >= 0;  // FAST on the raw plan (no canonicalisation pass)
+  GatherArgs g{};
   g.feat = f.data;
   if (c_count <= 0) {
     c_off = 0;
@@ -733,33 +804,44 @@ cudaError_t launch_gather_exact(const msda_features_t& f, const msda_csr_plan_t&
   g.empty = empty;
   g.one2 = make_float2(1.0f, 1.0f);
   g.nz2 = make_float2(-0.0f, -0.0f);
+  g.cam = p.camera_index;
+  g.lvl = p.level;
+  g.u = p.u;
+  g.v = p.v;
+  g.w = p.weight;
+  g.shape = f.spatial_shape;
+  g.start = f.scale_start_index;
+  g.n_cams = f.n_cams;
+  g.n_levels = f.n_levels;
+  g.normalize = raw ? fast_normalize : 0;
+  g.status = w.status;
   const size_t esz = f.dtype == MSDA_F32 ? 4 : 2;
   // vector width must divide the slice and keep every row (and output) access aligned
   const uintptr_t base = reinterpret_cast<uintptr_t>(f.data) | ((size_t)c_off * esz) | ((size_t)f.channels * esz);
   const uintptr_t obase = reinterpret_cast<uintptr_t>(out) | ((size_t)c_off * 4) | ((size_t)f.channels * 4);
   const int C = c_count;
   if (precision == MSDA_EXACT_HALF) {
-    if (C % 128 == 0 && base % 8 == 0) return launch_gather<__half, 4, true>(g, stream);
-    if (C % 8 == 0 && base % 16 == 0) return launch_gather<__half, 8, true>(g, stream);
-    if (C % 4 == 0 && base % 8 == 0) return launch_gather<__half, 4, true>(g, stream);
-    return launch_gather<__half, 2, true>(g, stream);
+    if (C % 128 == 0 && base % 8 == 0) return launch_gather<__half, 4, true>(g, stream, raw);
+    if (C % 8 == 0 && base % 16 == 0) return launch_gather<__half, 8, true>(g, stream, raw);
+    if (C % 4 == 0 && base % 8 == 0) return launch_gather<__half, 4, true>(g, stream, raw);
+    return launch_gather<__half, 2, true>(g, stream, raw);
   }
   switch (f.dtype) {
     case MSDA_F32:
       // two warps per 256 channels (16-B lanes) or, with MSDA_F32_LANE_BYTES=8, four (8-B lanes)
-      if (f32_lane_bytes() == 8 && C % 64 == 0 && base % 8 == 0) return launch_gather<float, 2, false>(g, stream);
-      if (C % 4 == 0 && base % 16 == 0 && obase % 16 == 0) return launch_gather<float, 4, false>(g, stream);
-      return launch_gather<float, 2, false>(g, stream);
+      if (f32_lane_bytes() == 8 && C % 64 == 0 && base % 8 == 0) return launch_gather<float, 2, false>(g, stream, raw);
+      if (C % 4 == 0 && base % 16 == 0 && obase % 16 == 0) return launch_gather<float, 4, false>(g, stream, raw);
+      return launch_gather<float, 2, false>(g, stream, raw);
     case MSDA_F16:
-      if (C % 128 == 0 && base % 8 == 0) return launch_gather<__half, 4, false>(g, stream);
-      if (C % 8 == 0 && base % 16 == 0) return launch_gather<__half, 8, false>(g, stream);
-      if (C % 4 == 0 && base % 8 == 0) return launch_gather<__half, 4, false>(g, stream);
-      return launch_gather<__half, 2, false>(g, stream);
+      if (C % 128 == 0 && base % 8 == 0) return launch_gather<__half, 4, false>(g, stream, raw);
+      if (C % 8 == 0 && base % 16 == 0) return launch_gather<__half, 8, false>(g, stream, raw);
+      if (C % 4 == 0 && base % 8 == 0) return launch_gather<__half, 4, false>(g, stream, raw);
+      return launch_gather<__half, 2, false>(g, stream, raw);
     default:
-      if (C % 128 == 0 && base % 8 == 0) return launch_gather<__nv_bfloat16, 4, false>(g, stream);
-      if (C % 8 == 0 && base % 16 == 0) return launch_gather<__nv_bfloat16, 8, false>(g, stream);
-      if (C % 4 == 0 && base % 8 == 0) return launch_gather<__nv_bfloat16, 4, false>(g, stream);
-      return launch_gather<__nv_bfloat16, 2, false>(g, stream);
+      if (C % 128 == 0 && base % 8 == 0) return launch_gather<__nv_bfloat16, 4, false>(g, stream, raw);
+      if (C % 8 == 0 && base % 16 == 0) return launch_gather<__nv_bfloat16, 8, false>(g, stream, raw);
+      if (C % 4 == 0 && base % 8 == 0) return launch_gather<__nv_bfloat16, 4, false>(g, stream, raw);
+      return launch_gather<__nv_bfloat16, 2, false>(g, stream, raw);
   }
 }
 

@@ -220,3 +220,41 @@ def test_errors_match_reference(cuda_dev):
     assert list(empty) == [True, False, True]
     assert not out[0].any() and not out[2].any()
     np.testing.assert_array_equal(out[1], grids[(0, 0)][1, 1])  # renormalised single weight is exactly 1
+
+
+@pytest.mark.parametrize("dt,channels,normalize", [("float32", 256, True), ("float32", 256, False),
+                                                   ("float16", 256, True), ("bfloat16", 512, True),
+                                                   ("float32", 64, True)])
+def test_fast_csr_skips_canonicalisation(c_oracle, cuda_dev, dt, channels, normalize):
+    """precision="fast" on the CSR plan: one gather launch straight from the
+    raw plan (any order, fused products) — within 1e-4 of the exact bytes
+    (north_star's fp32 bar; the features the GPU sees for f16/bf16), empty
+    queries flagged, data-dependent errors still raised.  C = 64 takes the
+    exact fallback."""
+    import torch
+
+    from paper_2601_10819_b200 import ops
+    from paper_2601_10819_b200.errors import NonFiniteWeight
+    from paper_2601_10819_b200.workload import BenchWorkload, generate_workload
+
+    wl = BenchWorkload(cameras=4, levels=4, channels=channels, queries=60, points_per_query=13,
+                       level0_size=(40, 96))
+    gw = generate_workload(wl)
+    offsets = np.concatenate([[0, 0], gw.offsets[1:]]).astype(np.int64)  # query 0 empty
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(cuda_dev)  # noqa: E731
+    table = t(gw.table).to(getattr(torch, dt))
+    feats = ops.DeviceFeatures(table, t(gw.spatial_shape), t(gw.tile_start.reshape(wl.cameras, wl.levels)))
+    args = (t(offsets), t(gw.camera_ids), t(gw.levels), t(gw.us), t(gw.vs), t(gw.weights))
+    fast, fe = ops.msda_csr(feats, *args, precision="fast", normalize=normalize)
+    exact, ee = ops.msda_csr(feats, *args, precision="exact", normalize=normalize)
+    fast, exact = fast.cpu().numpy(), exact.cpu().numpy()
+    assert np.array_equal(fe.cpu().numpy(), ee.cpu().numpy()) and bool(fe[0]) and not fast[0].any()
+    assert np.abs(fast - exact).max() / np.abs(exact).max() <= 1e-4
+    bad = gw.weights.copy()
+    bad[5] = np.nan
+    with pytest.raises(NonFiniteWeight):
+        ops.msda_csr(feats, *args[:5], t(bad), precision="fast")
+    zero = gw.weights.copy()
+    zero[int(offsets[3]):int(offsets[4])] = 0.0
+    with pytest.raises(ValueError, match="sum to zero"):
+        ops.msda_csr(feats, *args[:5], t(zero), precision="fast")
