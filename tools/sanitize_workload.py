@@ -1,0 +1,50 @@
+# compute-sanitizer workload: one small call of every production kernel (exact / fast / exact_half CSR,
+# dense fast / fast_h2 / exact, fused projection, OAE, visibility, painting, association) in f32 / f16 / bf16.
+# Run: compute-sanitizer --tool {memcheck,racecheck,synccheck,initcheck} python tools/sanitize_workload.py
+# Small invocations of every production kernel, for compute-sanitizer runs.
+import sys
+sys.path.insert(0, ".")
+import numpy as np
+import torch
+import __graft_entry__ as g
+g.smoke()  # exact CSR (plan + gather) + dense FAST
+from paper_2601_10819_b200 import ops
+from paper_2601_10819_b200.workload import BenchWorkload, generate_workload
+dev = torch.device("cuda", 0)
+wl = BenchWorkload(cameras=2, levels=4, channels=256, queries=16, points_per_query=13, level0_size=(32, 88))
+gw = generate_workload(wl)
+t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+for dt in (torch.float32, torch.float16, torch.bfloat16):
+    feats = ops.DeviceFeatures(t(gw.table).to(dt), t(gw.spatial_shape), t(gw.tile_start.reshape(2, 4)))
+    for prec in ("exact", "fast"):
+        ops.msda_csr(feats, t(gw.offsets), t(gw.camera_ids), t(gw.levels), t(gw.us), t(gw.vs), t(gw.weights), precision=prec)
+    if dt is torch.float16:
+        ops.msda_csr(feats, t(gw.offsets), t(gw.camera_ids), t(gw.levels), t(gw.us), t(gw.vs), t(gw.weights), precision="exact_half")
+    rng = np.random.default_rng(1)
+    loc = t(rng.uniform(0, 1, (1, 16, 13, 2, 2)).astype(np.float32))
+    w = t(rng.uniform(0.01, 1, (1, 16, 13, 2, 4, 8)).astype(np.float32))
+    for prec in ("fast", "fast_h2", "exact"):
+        if prec == "fast_h2" and dt is not torch.float16:
+            continue
+        ops.deformable_aggregation(feats, None, None, loc, w, precision=prec, normalize=True, check=True)
+    K = np.array([[300.0, 300.0, 352.0, 128.0]] * 2)
+    R = np.stack([np.eye(3), np.eye(3)]).reshape(2, 9)
+    T = np.array([[0.0, 0.0, 10.0], [0.0, 0.0, 12.0]])
+    cams = ops.Cameras(K, R, T, device=dev)
+    anchors = torch.zeros((1, 16, 10), device=dev)
+    anchors[..., 3:6] = torch.tensor([0.6, 0.6, 1.8])
+    offs = np.zeros((6, 3), np.float32)
+    wp = t(rng.uniform(0.01, 1, (1, 16, 13, 2, 4, 8)).astype(np.float32))
+    ops.msda_dense_project(feats, anchors, offs, cams, [4.0, 8.0, 16.0, 32.0], wp, check=True)
+    desc = torch.randn((16, 256), device=dev)
+    vis = torch.rand((16, 2), device=dev)
+    mem = torch.nn.functional.normalize(torch.randn((16, 256), device=dev), dim=1)
+    ops.oae_pool(feats, anchors[0], offs, cams, [4.0, 8.0, 16.0, 32.0], desc, vis, mem)
+ops.visibility(cams, [[704, 256]] * 2, [[0, 0, 0, 1, 1, 1, 0], [0.5, 0, 1, 1, 1, 1, 0.3]], grid=16)
+sc = ops.PaintScene(cams, [[704, 256]] * 2, [8.0, 16.0], 32, [[0, 0, 0, 1, 1, 1, 0], [0.5, 0, 1, 1, 1, 1, 0.3]], 1,
+                    np.ones((1, 32)) / np.sqrt(32))
+sc.run(seed=3)
+sc.run(background=np.zeros((sc.rows, 32)))
+ops.association_cost(np.zeros((20, 3)), np.ones((17, 3)), np.random.rand(20, 130), np.random.rand(17, 130), device=dev)
+torch.cuda.synchronize()
+print("sanitizer workload done")
