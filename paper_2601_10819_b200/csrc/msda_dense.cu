@@ -476,6 +476,117 @@ __global__ void dense_expand_kernel(DenseArgs a, int group, int64_t* offsets, in
   }
 }
 
+// ---------------------------------------------------------------------------
+// EXACT with channel groups in one pass.  The canonical order (camera, level,
+// v, u, w; features.py:261-263) differs between groups only among samples
+// whose (camera, level, v, u) tie — and tied samples share one bilinear
+// record — so one canonicalisation serves every group: records are written
+// once at the shared slot; each group's weight goes to its own slot, the
+// tied ones ranked by that group's weight (then position).  Per-group
+// sequential f32 weight sums (threads 0..G-1, in each group's canonical
+// order) normalise in place, and one gather over all channels reads the
+// lane's group weight: bit-identical to G separate plans.
+// Samples are indexed i = (camera * L + level) * P + point, so the
+// (camera, level) run of i is [i - i % P, i - i % P + P).
+
+template <bool PROJECT>
+__global__ void __launch_bounds__(128) dense_canon_kernel(DenseArgs a, SampleRec* rec, float* wn, int normalize) {
+  extern __shared__ __align__(16) unsigned long long s_kp[];  // [n] (ord(v) << 32) | ord(u), then [n] valid bytes
+  __shared__ double s_kpt[PROJECT ? kMaxPoints * 3 : 1];
+  __shared__ float s_ws[kMaxGroups];
+  const int n = a.P * a.cams * a.L;
+  const int64_t bq = blockIdx.x;
+  const int b = (int)(bq / a.Q);
+  const int64_t lo = bq * n;
+  const int G = a.G;
+  const int64_t row_base = (int64_t)b * a.n_rows;
+  unsigned char* s_valid = reinterpret_cast<unsigned char*>(s_kp + n);
+  if constexpr (PROJECT) {
+    anchor_keypoints(a, bq, s_kpt, a.status);
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int p = i % a.P, t = i / a.P, cam = t / a.L, l = t - cam * a.L;
+    float u, v;
+    bool valid = true;
+    if constexpr (PROJECT) {
+      double up, vp;
+      valid = project_point(a, cam, s_kpt + 3 * p, up, vp);
+      if (valid) {
+        const double st = (double)a.strides[l];
+        u = (float)(up / st - 0.5);
+        v = (float)(vp / st - 0.5);
+      } else {  // behind the camera: outside every grid and weight 0 (the plan keeps it, it adds nothing)
+        u = v = -4.0f;
+      }
+    } else {
+      const float* lp = a.loc + ((bq * a.P + p) * a.cams + cam) * 2;
+      u = __fsub_rn(__fmul_rn(lp[0], (float)a.shape[2 * t + 1]), 0.5f);
+      v = __fsub_rn(__fmul_rn(lp[1], (float)a.shape[2 * t]), 0.5f);
+    }
+    s_kp[i] = ((unsigned long long)ord_f32(v) << 32) | ord_f32(u);
+    s_valid[i] = valid ? 1 : 0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int p = i % a.P, t = i / a.P, cam = t / a.L, l = t - cam * a.L;
+    const int r0 = i - p;
+    const unsigned long long ki = s_kp[i];
+    int below = 0;
+    bool tie = false;
+    for (int j = r0; j < r0 + a.P; ++j) {
+      const unsigned long long kj = s_kp[j];
+      below += kj < ki ? 1 : 0;
+      tie |= (kj == ki) & (j != i);
+    }
+    const float u = unord_f32((uint32_t)(ki & 0xffffffffu)), v = unord_f32((uint32_t)(ki >> 32));
+    const bool valid = s_valid[i] != 0;
+    const int slot = r0 + below;  // first slot of this (v, u) value inside the run
+    const float* wp = a.w + (((bq * a.P + p) * a.cams + cam) * a.L + l) * (int64_t)G;
+    int eq_before = 0;  // rank among exact (v, u) ties by position: tied records are identical
+    if (tie)
+      for (int j = r0; j < i; ++j) eq_before += s_kp[j] == ki ? 1 : 0;
+    rec[lo + slot + eq_before] = make_record(u, v, row_base + a.start[t], a.shape[2 * t], a.shape[2 * t + 1]);
+    for (int g = 0; g < G; ++g) {
+      const float wg = valid ? __ldg(wp + g) : 0.0f;
+      int sg = slot;
+      if (tie) {  // rank inside the tie by this group's weight, then position
+        const uint32_t oi = ord_f32(wg);
+        for (int j = r0; j < r0 + a.P; ++j) {
+          if (j == i || s_kp[j] != ki) continue;
+          const float* wpj = a.w + (((bq * a.P + (j - r0)) * a.cams + cam) * a.L + l) * (int64_t)G;
+          const uint32_t oj = ord_f32(s_valid[j] ? __ldg(wpj + g) : 0.0f);
+          sg += (oj < oi || (oj == oi && j < i)) ? 1 : 0;
+        }
+      }
+      wn[(lo + sg) * G + g] = wg;
+    }
+  }
+  __syncthreads();
+  if (normalize) {
+    if (threadIdx.x < G) {  // sequential f32 sum in this group's canonical order (features.py:264-269)
+      float ws = 0.0f;
+      const float* wg = wn + lo * G + threadIdx.x;
+      for (int s2 = 0; s2 < n; ++s2) ws = __fadd_rn(ws, wg[(int64_t)s2 * G]);
+      if (ws == 0.0f) set_status(a.status, MSDA_ZERO_WEIGHT_SUM, bq);
+      s_ws[threadIdx.x] = ws;
+    }
+    __syncthreads();
+    for (int64_t k = threadIdx.x; k < (int64_t)n * G; k += blockDim.x)
+      wn[lo * G + k] = __fdiv_rn(wn[lo * G + k], s_ws[k % G]);
+  }
+}
+
+__global__ void dense_offsets_kernel(int64_t* off, int64_t nq, int n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= nq; i += (int64_t)gridDim.x * blockDim.x)
+    off[i] = i * n;
+}
+
+cudaError_t launch_dense_offsets(int64_t* off, int64_t nq, int n, cudaStream_t s) {
+  dense_offsets_kernel<<<(unsigned)std::min<int64_t>((nq + 256) / 256, 1024), 256, 0, s>>>(off, nq, n);
+  return cudaGetLastError();
+}
+
 size_t dense_exact_extra_bytes(int64_t n_queries, int64_t n_samples) {
   return align_up((size_t)(n_queries + 1) * 8, 256) + 5 * align_up((size_t)n_samples * 4, 256);
 }
@@ -560,6 +671,31 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
     return e == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
   }
   if (precision == MSDA_EXACT_HALF && f->dtype != MSDA_F16) return MSDA_BAD_ARG;
+  {  // EXACT, one pass for every group (bit-identical to the per-group plans below)
+    const int n = P * a.cams * a.L;
+    const size_t smem = (size_t)n * 9;
+    SampleRec* rec = ew.rec;
+    float* wn_g = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + exact_workspace_bytes(nq, S) +
+                                           dense_exact_extra_bytes(nq, S));
+    if (G <= 8 && smem <= 200 * 1024 && ws_bytes >= dense_ws(a.bs, Q, P, a.cams, a.L) + (size_t)S * G * 4) {
+      msda_csr_plan_t plan1{nq, S, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+      // offsets: every query owns n consecutive canonical slots
+      int64_t* d_off = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(ws) + exact_workspace_bytes(nq, S));
+      plan1.offsets = d_off;
+      if (launch_dense_offsets(d_off, nq, n, s) != cudaSuccess) return MSDA_CUDA_ERROR;
+      auto kern = project ? dense_canon_kernel<true> : dense_canon_kernel<false>;
+      if (smem > 48 * 1024 &&
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return MSDA_CUDA_ERROR;
+      kern<<<(unsigned)nq, 128, smem, s>>>(a, rec, wn_g, normalize);
+      if (cudaGetLastError() != cudaSuccess) return MSDA_CUDA_ERROR;
+      ExactWorkspace ew1 = ew;
+      ew1.wn = wn_g;
+      const cudaError_t e = launch_gather_exact(*f, plan1, precision, ew1, out, nullptr, s, 0, 0, -1, G);
+      if (e == cudaSuccess) return MSDA_OK;
+      if (e != cudaErrorNotSupported) return MSDA_CUDA_ERROR;
+    }
+  }
   // EXACT / EXACT_HALF: one canonical CSR plan per group, exact kernels on its channel slice
   char* p = reinterpret_cast<char*>(ws) + exact_workspace_bytes(nq, S);
   int64_t* d_off = reinterpret_cast<int64_t*>(p);
@@ -595,9 +731,9 @@ extern "C" {
 
 size_t msda_dense_workspace_size(int32_t batch, int32_t n_queries, int32_t n_points, int32_t n_cams,
                                  int32_t n_levels, int32_t n_groups, int32_t channels) {
-  (void)n_groups;
   (void)channels;
-  return dense_ws(batch, n_queries, n_points, n_cams, n_levels);
+  const int64_t S = (int64_t)batch * n_queries * n_points * n_cams * n_levels;
+  return dense_ws(batch, n_queries, n_points, n_cams, n_levels) + (size_t)S * std::max(1, (int)n_groups) * 4;
 }
 
 int32_t msda_dense(const msda_features_t* feat, int32_t n_queries, int32_t n_points, int32_t n_groups,

@@ -310,6 +310,8 @@ struct GatherArgs {
   const int64_t* start;
   int32_t n_cams, n_levels, normalize;
   DevStatus* status;
+  // dense EXACT with channel groups: wn is [S, n_groups], channel c uses group c / cpg
+  int32_t n_groups, cpg;
 };
 
 __device__ __forceinline__ SampleRec ld_rec(const SampleRec* p) {
@@ -461,13 +463,13 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N));
 }
 
-template <int BYTES, int D>
+template <int BYTES, int D, int GW = 1>
 struct PipeSmem {
   static constexpr int kSlot = 4 * 32 * BYTES;  // one sample: 4 corners x 32 lanes
   static constexpr int kCorner = D * kSlot;      // corner ring
   static constexpr int kRows = 2 * 32 * 16;      // int4 rows[2][32]
   static constexpr int kIw = 2 * 32 * 16;        // float4 iw[2][32]
-  static constexpr int kWn = 2 * 32 * 4;         // float wn[2][32]
+  static constexpr int kWn = 2 * 32 * 4 * GW;    // float wn[2][32][GW] (GW weights per sample: channel groups)
   static constexpr int kPerWarp = kCorner + kRows + kIw + kWn;
 };
 
@@ -492,10 +494,10 @@ __device__ __forceinline__ void fast_accumulate(float* acc, const float (*c)[VEC
 // RAW = FAST on the CSR plan: records are built from the plan arrays in the
 // batch loader and the weight sum is a warp reduction (any order), so no
 // canonicalisation pass runs; the gather pipeline is the exact path's.
-template <typename T, int VEC, bool HALF, int D, bool RAW>
+template <typename T, int VEC, bool HALF, int D, bool RAW, int GW>
 __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs a) {
   constexpr int BYTES = VEC * (int)sizeof(T);
-  using SM = PipeSmem<BYTES, D>;
+  using SM = PipeSmem<BYTES, D, GW>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* base = smem_raw + warp * SM::kPerWarp;
@@ -513,7 +515,8 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   const int64_t lo = a.offsets[q];
   const int n = (int)(a.offsets[q + 1] - lo);
   const SampleRec* rec = a.rec + lo;
-  const float* wnp = a.wn + lo;
+  const float* wnp = a.wn + lo * (GW > 1 ? a.n_groups : 1);
+  const int gl = GW > 1 ? (a.c_off + c0) / a.cpg : 0;  // this lane's channel group
   const char* featc = reinterpret_cast<const char*>(a.feat) + (size_t)(a.c_off + c0) * sizeof(T);
   const uint32_t row_bytes = (uint32_t)a.row_elems * (uint32_t)sizeof(T);
 
@@ -534,6 +537,9 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   int4 r_rows = make_int4(-1, -1, -1, -1);
   float4 r_iw = make_float4(0.f, 0.f, 0.f, 0.f);
   float r_wn = 0.0f;
+  float r_wg[GW];
+#pragma unroll
+  for (int k = 0; k < GW; ++k) r_wg[k] = 0.0f;
   auto load_batch = [&](int b) {
     const int s = b * 32 + lane;
     if (s < n) {
@@ -553,7 +559,13 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
         r_wn = a.normalize ? ww / wsum : ww;
       } else {
         r = ld_rec(rec + s);
-        r_wn = __ldg(wnp + s);
+        if constexpr (GW == 1) {
+          r_wn = __ldg(wnp + s);
+        } else {
+#pragma unroll
+          for (int k = 0; k < GW; ++k)
+            if (k < a.n_groups) r_wg[k] = __ldg(wnp + (int64_t)s * a.n_groups + k);
+        }
       }
       r_rows = make_int4(r.row[0], r.row[1], r.row[2], r.row[3]);
       r_iw = make_float4(r.iw[0], r.iw[1], r.iw[2], r.iw[3]);
@@ -562,7 +574,12 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   auto store_batch = [&](int buf) {
     s_rows[buf * 32 + lane] = r_rows;
     s_iw[buf * 32 + lane] = r_iw;
-    s_wn[buf * 32 + lane] = r_wn;
+    if constexpr (GW == 1) {
+      s_wn[buf * 32 + lane] = r_wn;
+    } else {
+#pragma unroll
+      for (int k = 0; k < GW; ++k) s_wn[(buf * 32 + lane) * GW + k] = r_wg[k];
+    }
   };
   auto issue = [&](int k, uint32_t slot_off) {
     const int4 rows = s_rows[((k >> 5) & 1) * 32 + (k & 31)];
@@ -601,7 +618,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
     const int b0 = ((i >> 5) & 1) * 32 + (i & 31);
     const int b1 = (((i + 1) >> 5) & 1) * 32 + ((i + 1) & 31);
     const float4 iw0 = s_iw[b0], iw1 = s_iw[b1];
-    const float wn0 = s_wn[b0], wn1 = s_wn[b1];
+    const float wn0 = s_wn[b0 * GW + gl], wn1 = s_wn[b1 * GW + gl];
     const uint32_t off1 = (read_off + SM::kSlot == (uint32_t)SM::kCorner) ? 0u : read_off + SM::kSlot;
     RawVec<BYTES> cv0[4], cv1[4];
 #pragma unroll
@@ -670,13 +687,13 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   if (c0 == 0 && a.empty) a.empty[q] = (n == 0) ? 1 : 0;
 }
 
-template <typename T, int VEC, bool HALF, int D, bool RAW>
+template <typename T, int VEC, bool HALF, int D, bool RAW, int GW = 1>
 cudaError_t launch_gather_pipe(const GatherArgs& g, cudaStream_t stream) {
   constexpr int BYTES = VEC * (int)sizeof(T);
-  const int smem = kPipeWarps * PipeSmem<BYTES, D>::kPerWarp;
+  const int smem = kPipeWarps * PipeSmem<BYTES, D, GW>::kPerWarp;
   static bool attr_set = false;  // per instantiation; idempotent
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gather_pipe_kernel<T, VEC, HALF, D, RAW>,
+    cudaError_t e = cudaFuncSetAttribute(gather_pipe_kernel<T, VEC, HALF, D, RAW, GW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
@@ -684,12 +701,17 @@ cudaError_t launch_gather_pipe(const GatherArgs& g, cudaStream_t stream) {
   const int64_t warps = g.n_queries * (g.C / VEC / 32);
   const int64_t grid = (warps + kPipeWarps - 1) / kPipeWarps;
   if (grid == 0) return cudaSuccess;
-  gather_pipe_kernel<T, VEC, HALF, D, RAW><<<(unsigned)grid, kPipeWarps * 32, smem, stream>>>(g);
+  gather_pipe_kernel<T, VEC, HALF, D, RAW, GW><<<(unsigned)grid, kPipeWarps * 32, smem, stream>>>(g);
   return cudaGetLastError();
 }
 
 template <typename T, int VEC, bool HALF>
 cudaError_t launch_gather(const GatherArgs& g, cudaStream_t stream, bool raw) {
+  if (g.n_groups > 1) {  // per-group weights (dense EXACT, one pass): pipelined kernel only
+    if ((g.C / VEC) % 32 != 0 || g.C % VEC != 0 || g.n_groups > 8) return cudaErrorNotSupported;
+    if constexpr (VEC * sizeof(T) == 16) return launch_gather_pipe<T, VEC, HALF, 7, false, 8>(g, stream);
+    else return launch_gather_pipe<T, VEC, HALF, 12, false, 8>(g, stream);
+  }
   if ((g.C / VEC) % 32 == 0 && g.C % VEC == 0) {
     if constexpr (!HALF) {
       if (raw) {
@@ -784,9 +806,11 @@ cudaError_t launch_plan_canon(const msda_features_t& f, const msda_csr_plan_t& p
 
 cudaError_t launch_gather_exact(const msda_features_t& f, const msda_csr_plan_t& p, int precision,
                                 const ExactWorkspace& w, float* out, uint8_t* empty, cudaStream_t stream,
-                                int c_off, int c_count, int fast_normalize) {
+                                int c_off, int c_count, int fast_normalize, int n_groups) {
   const bool raw = fast_normalize >= 0;  // FAST on the raw plan (no canonicalisation pass)
   GatherArgs g{};
+  g.n_groups = n_groups;
+  g.cpg = f.channels / std::max(1, n_groups);
   g.feat = f.data;
   if (c_count <= 0) {
     c_off = 0;

@@ -21,7 +21,7 @@ cudaError_t launch_plan_canon(const msda_features_t& f, const msda_csr_plan_t& p
                               int64_t queries_per_batch = 0);
 cudaError_t launch_gather_exact(const msda_features_t& f, const msda_csr_plan_t& p, int precision,
                                 const ExactWorkspace& w, float* out, uint8_t* empty, cudaStream_t stream,
-                                int c_off = 0, int c_count = 0, int fast_normalize = -1);
+                                int c_off = 0, int c_count = 0, int fast_normalize = -1, int n_groups = 1);
 // FAST on the CSR plan: one gather launch straight from the raw plan arrays
 // (fast_normalize = normalize flag); cudaErrorNotSupported when the channel
 // slice does not span whole warps (the caller then runs the exact stages).

@@ -303,3 +303,30 @@ def test_dense_slice_kernel(cuda_dev, dt, precision, normalize, channels, groups
     ref = mo.msda_dense_groups(seen, tiles, shape, loc, wts, 4, normalize=normalize)
     tol = 1e-2 if precision == "fast_h2" else 1e-4
     assert rel(out, ref) <= tol
+
+
+@pytest.mark.parametrize("dt,groups,normalize", [("float32", 8, True), ("float32", 8, False), ("float32", 1, True),
+                                                 ("float32", 4, True), ("float16", 8, True), ("bfloat16", 2, False)])
+def test_dense_exact_one_pass_with_ties(cuda_dev, dt, groups, normalize):
+    """EXACT with channel groups canonicalises once for every group: samples
+    whose (camera, level, v, u) tie are ordered per group by that group's
+    weight.  Duplicated sampling points (exact ties, with and without equal
+    weights) must still give the per-group reference bytes."""
+    import torch
+
+    from paper_2601_10819_b200 import ops
+
+    rng = np.random.default_rng(17 + groups)
+    grids, shape, loc, wts = helpers.make_dense(rng, bs=2, n_q=9, n_p=13, cams=3, n_levels=4, groups=groups,
+                                                channels=256, size_lo=6, size_hi=20)
+    loc[:, :, 5] = loc[:, :, 2]  # point 5 duplicates point 2 in every camera: (v, u) ties in every level
+    loc[:, :, 9] = loc[:, :, 2]
+    wts[:, :, 9] = wts[:, :, 2]  # ... one duplicate with the very same weights
+    wts[0, 3, 5, :, :, 0] = wts[0, 3, 2, :, :, 0]  # equal weight in one group only
+    feats, table, tiles = _feats(ops, torch, grids, shape, cuda_dev, dtype=getattr(torch, dt), batch=2)
+    seen = feats.table[0].float().cpu().numpy()
+    t = lambda a: torch.from_numpy(a).to(cuda_dev)  # noqa: E731
+    out = ops.deformable_aggregation(feats, None, None, t(loc), t(wts), precision="exact", normalize=normalize,
+                                     check=True).cpu().numpy()
+    ref = mo.msda_dense_groups(seen, tiles, shape, loc, wts, 4, normalize=normalize)
+    assert out.tobytes() == ref.tobytes()
