@@ -75,7 +75,21 @@ def touched_bytes(feats, loc, esize):
                     ok = (x >= 0) & (x < W) & (y >= 0) & (y < H)
                     b = torch.arange(bs, device=loc.device).view(bs, 1, 1).expand_as(x)
                     idx.append((b * feats.table.shape[1] + int(start[c, m]) + y * W + x)[ok])
-    return torch.unique(torch.cat(idx)).numel() * feats.channels * esize
+    rows = torch.cat(idx)
+    # (unique touched bytes, bytes of every in-grid corner row the kernel moves L2 -> SM)
+    return torch.unique(rows).numel() * feats.channels * esize, rows.numel() * feats.channels * esize
+
+
+def l2_ceiling():
+    """Measured L2 -> SM random-row gather ceiling (tools/gather_ceiling.cu)."""
+    p = ROOT / "profiles" / "r1" / "gather_ceiling.txt"
+    best = None
+    if p.exists():
+        for line in p.read_text().splitlines():
+            if line.startswith("pipe_") and "moved" in line:
+                v = float(line.split("moved")[1].split("GB/s")[0])
+                best = v if best is None else max(best, v)
+    return best
 
 
 def time_fn(fn, reps, flush):
@@ -105,16 +119,20 @@ def dense_case(name, cams, levels, C, G, dtype, precision, reps, dev, Q=900, P=1
     table_bytes = feats.table.numel() * esize
     fn = lambda: ops.deformable_aggregation(feats, None, None, loc, w, precision=precision, out=out)  # noqa: E731
     med, best = time_fn(fn, reps, flush=table_bytes < 2 * L2)
-    tb = touched_bytes(feats, loc, esize)
+    tb, moved = touched_bytes(feats, loc, esize)
     alg = tb + loc.numel() * 4 + w.numel() * 4 + out.numel() * 4
     gbs = alg / (med / 1e3) / 1e9
+    l2_gbs = moved / (med / 1e3) / 1e9
+    ceil = l2_ceiling()
     cams_total = bs * cams
     return {"config": name, "path": "deformable_aggregation", "precision": precision, "dtype": str(dtype),
             "cams": cams, "groups": G, "latency_us": med * 1e3, "best_us": best * 1e3,
             "algorithmic_bytes": alg, "touched_feature_bytes": tb, "achieved_gbs": gbs, "frac": gbs / peak(),
             "camera_frames_per_s": cams_total / (med / 1e3),
             "streams_at_30fps_6layers": int(cams_total / (30 * 6 * med / 1e3)),
-            "l2": "flushed" if table_bytes < 2 * L2 else "table > L2"}
+            "l2": "flushed" if table_bytes < 2 * L2 else "table > L2",
+            "l2_gather": {"bytes": moved, "achieved_gbs": l2_gbs, "ceiling_gbs": ceil,
+                          "frac": (l2_gbs / ceil) if ceil else None}}
 
 
 def ring(cams, radius=12.0, height=4.0, focal=300.0, size=(704, 256)):
