@@ -127,6 +127,17 @@ int32_t msda_dense(const msda_features_t *feat, int32_t n_queries, int32_t n_poi
                    const float *sampling_location, const float *weights, int32_t precision,
                    int32_t normalize, float *out, void *workspace, size_t workspace_bytes, void *stream);
 
+/* Camera-sharded partials (paper_2601_10819_b200/dist.py): FAST aggregation of
+ * this rank's cameras without normalisation, plus the per-(query, group)
+ * weight sums weight_sums [bs*Q, G]; after summing both across ranks (NCCL
+ * all-reduce), msda_dense_normalize divides out by the sums (zero sum ->
+ * MSDA_ZERO_WEIGHT_SUM in the workspace status word, msda_read_status).    */
+int32_t msda_dense_partial(const msda_features_t *feat, int32_t n_queries, int32_t n_points, int32_t n_groups,
+                           const float *sampling_location, const float *weights, int32_t precision, float *out,
+                           float *weight_sums, void *workspace, size_t workspace_bytes, void *stream);
+int32_t msda_dense_normalize(float *out, const float *weight_sums, int64_t n_queries, int32_t channels,
+                             int32_t n_groups, void *workspace /* >= 256 B */, void *stream);
+
 /* Fused projection: anchors [bs, Q, 10] (x, y, z, w, l, h, yaw, vx, vy, vz),
  * learned_offsets [n_learned, 3] in [-1, 1], P = 7 + n_learned keypoints
  * (geometry.py:207-247), motion compensation by velocity*dt

@@ -57,6 +57,8 @@ SIGNATURES = {
     "msda_csr_stages": (I32, [ctypes.POINTER(Features), ctypes.POINTER(CsrPlan), I32, I32, P, P, P, SZ, P, I32]),
     "msda_dense_workspace_size": (SZ, [I32, I32, I32, I32, I32, I32, I32]),
     "msda_dense": (I32, [ctypes.POINTER(Features), I32, I32, I32, P, P, I32, I32, P, P, SZ, P]),
+    "msda_dense_partial": (I32, [ctypes.POINTER(Features), I32, I32, I32, P, P, I32, P, P, P, SZ, P]),
+    "msda_dense_normalize": (I32, [P, P, I64, I32, I32, P, P]),
     "msda_dense_project": (I32, [ctypes.POINTER(Features), I32, P, I32, P, ctypes.POINTER(Cameras), P,
                                  ctypes.c_float, I32, P, I32, I32, P, P, SZ, P]),
     "msda_oae_pool": (I32, [ctypes.POINTER(Features), I32, P, I32, P, ctypes.POINTER(Cameras), P, P, P, P, P, P,

@@ -45,6 +45,7 @@ struct DenseArgs {
   const float* w;    // [bs, Q, P, cams, L, G]
   int32_t normalize;
   float* out;        // [bs, Q, C]
+  float* wsum_out;   // [bs, Q, G] per-(anchor, group) weight sums, or null (camera-sharded partials)
   DevStatus* status;
   // PROJECT mode
   const float* anchors;  // [bs, Q, 10]
@@ -203,12 +204,15 @@ __global__ void __launch_bounds__(kDenseThreads) dense_fast_kernel(DenseArgs a) 
   for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
     float sum = 0.0f;
     for (int j = 0; j < n_split; ++j) sum += s_red[j * a.C + c];
-    if (a.normalize) {
+    if (a.normalize || a.wsum_out) {
       const int gg = c / cpg;
       float ws = 0.0f;
       for (int j = 0; j < n_split; ++j) ws += s_wsum[j * a.G + gg];
-      if (ws == 0.0f) set_status(a.status, MSDA_ZERO_WEIGHT_SUM, bq);
-      sum = sum / ws;
+      if (a.wsum_out && c == gg * cpg) a.wsum_out[bq * a.G + gg] = ws;
+      if (a.normalize) {
+        if (ws == 0.0f) set_status(a.status, MSDA_ZERO_WEIGHT_SUM, bq);
+        sum = sum / ws;
+      }
     }
     o[c] = sum;
   }
@@ -361,13 +365,16 @@ __global__ void __launch_bounds__(kWcWarps * 32) dense_warpcam_kernel(DenseArgs 
     float sum = 0.0f;
 #pragma unroll
     for (int j = 0; j < kWcWarps; ++j) sum += s_red[j][c];
-    if (a.normalize) {
+    if (a.normalize || a.wsum_out) {
       const int gg = c / cpg;
       float ws = 0.0f;
 #pragma unroll
       for (int j = 0; j < kWcWarps; ++j) ws += s_ws[j][gg];
-      if (ws == 0.0f) set_status(a.status, MSDA_ZERO_WEIGHT_SUM, bq);
-      sum = sum / ws;
+      if (a.wsum_out && c == gg * cpg) a.wsum_out[bq * a.G + gg] = ws;
+      if (a.normalize) {
+        if (ws == 0.0f) set_status(a.status, MSDA_ZERO_WEIGHT_SUM, bq);
+        sum = sum / ws;
+      }
     }
     o[c] = sum;
   }
@@ -587,6 +594,17 @@ cudaError_t launch_dense_offsets(int64_t* off, int64_t nq, int n, cudaStream_t s
   return cudaGetLastError();
 }
 
+// out[q, c] /= weight_sums[q, c / (C / G)] (camera-sharded partials after the all-reduce)
+__global__ void group_normalize_kernel(float* out, const float* wsum, int64_t n_q, int C, int G, DevStatus* st) {
+  const int cpg = C / G;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_q * C; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = i / C;
+    const float ws = wsum[q * G + (int)(i - q * C) / cpg];
+    if (ws == 0.0f) set_status(st, MSDA_ZERO_WEIGHT_SUM, q);
+    out[i] = out[i] / ws;
+  }
+}
+
 size_t dense_exact_extra_bytes(int64_t n_queries, int64_t n_samples) {
   return align_up((size_t)(n_queries + 1) * 8, 256) + 5 * align_up((size_t)n_samples * 4, 256);
 }
@@ -594,7 +612,7 @@ size_t dense_exact_extra_bytes(int64_t n_queries, int64_t n_samples) {
 int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, const float* loc, const float* w,
                   int32_t precision, int32_t normalize, float* out, void* ws, size_t ws_bytes, cudaStream_t s,
                   bool project, const float* anchors, int32_t n_learned, const float* offsets,
-                  const msda_cameras_t* cams, const float* strides, float dt);
+                  const msda_cameras_t* cams, const float* strides, float dt, float* wsum_out = nullptr);
 
 }  // namespace
 }  // namespace msda
@@ -630,8 +648,9 @@ namespace {
 int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, const float* loc, const float* w,
                   int32_t precision, int32_t normalize, float* out, void* ws, size_t ws_bytes, cudaStream_t s,
                   bool project, const float* anchors, int32_t n_learned, const float* offsets,
-                  const msda_cameras_t* cams, const float* strides, float dt) {
+                  const msda_cameras_t* cams, const float* strides, float dt, float* wsum_out) {
   DenseArgs a{};
+  a.wsum_out = wsum_out;
   a.feat = f->data;
   a.n_rows = f->n_rows;
   a.C = f->channels;
@@ -746,6 +765,33 @@ int32_t msda_dense(const msda_features_t* feat, int32_t n_queries, int32_t n_poi
   return run_dense(feat, n_queries, n_points, n_groups, sampling_location, weights, precision, normalize, out,
                    workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream), false, nullptr, 0, nullptr,
                    nullptr, nullptr, 0.0f);
+}
+
+int32_t msda_dense_partial(const msda_features_t* feat, int32_t n_queries, int32_t n_points, int32_t n_groups,
+                           const float* sampling_location, const float* weights, int32_t precision, float* out,
+                           float* weight_sums, void* workspace, size_t workspace_bytes, void* stream) {
+  int32_t st = validate_dense(feat, n_queries, n_points, n_groups);
+  if (st != MSDA_OK) return st;
+  if (precision != MSDA_FAST && precision != MSDA_FAST_H2) return MSDA_BAD_PRECISION;
+  if (!sampling_location || !weights || !out || !weight_sums || !workspace) return MSDA_BAD_ARG;
+  return run_dense(feat, n_queries, n_points, n_groups, sampling_location, weights, precision, 0, out, workspace,
+                   workspace_bytes, reinterpret_cast<cudaStream_t>(stream), false, nullptr, 0, nullptr, nullptr,
+                   nullptr, 0.0f, weight_sums);
+}
+
+int32_t msda_dense_normalize(float* out, const float* weight_sums, int64_t n_queries, int32_t channels,
+                             int32_t n_groups, void* workspace, void* stream) {
+  if (!out || !weight_sums || !workspace || n_queries < 0 || channels <= 0 || n_groups <= 0 ||
+      channels % n_groups)
+    return MSDA_BAD_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  DevStatus* status = reinterpret_cast<DevStatus*>(workspace);
+  if (cudaMemsetAsync(status, 0, sizeof(DevStatus), s) != cudaSuccess) return MSDA_CUDA_ERROR;
+  if (n_queries == 0) return MSDA_OK;
+  const int64_t total = n_queries * channels;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+  group_normalize_kernel<<<blocks, 256, 0, s>>>(out, weight_sums, n_queries, channels, n_groups, status);
+  return cudaGetLastError() == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
 }
 
 int32_t msda_dense_project(const msda_features_t* feat, int32_t n_queries, const float* anchors, int32_t n_learned,

@@ -39,15 +39,18 @@ def shard_streams(n_scenes: int, rank: int, world: int) -> list[int]:
 class CameraShardedAggregation:
     """Sparse4D deformable aggregation of one scene with cameras across ranks.
 
-    ``local_fn(loc, weights)`` aggregates this rank's cameras with
-    ``normalize=False`` and returns ``[bs, Q, C]`` float32 on the rank's
-    device; on GPUs it is ``ops.deformable_aggregation`` bound to the rank's
-    feature table (see :meth:`for_device_features`).
+    ``local_fn(loc, weights)`` aggregates this rank's cameras without
+    normalisation and returns ``[bs, Q, C]`` float32 — or ``(out, weight_sums
+    [bs, Q, G])``.  On GPUs it is the C-ABI ``msda_dense_partial`` bound to
+    the rank's feature table and ``normalize_fn`` is ``msda_dense_normalize``
+    (see :meth:`for_device_features`), so no arithmetic runs outside the
+    library; the CPU tests pass a numpy stand-in and fall back to torch.
     """
 
     n_cams: int
     local_fn: Callable
     group: object = None
+    normalize_fn: Callable | None = None
 
     def __post_init__(self):
         self.rank = dist.get_rank(self.group) if dist.is_initialized() else 0
@@ -63,23 +66,28 @@ class CameraShardedAggregation:
         else:
             loc = sampling_location[:, :, :, self.cam_lo:self.cam_hi].contiguous()
             wts = weights[:, :, :, self.cam_lo:self.cam_hi].contiguous()
-        part = self.local_fn(loc, wts)
+        res = self.local_fn(loc, wts)
+        part, wsum = res if isinstance(res, tuple) else (res, None)
         bs, q_n, c_n = part.shape
         g_n = weights.shape[-1]
         if normalize:
-            wsum = wts.sum(dim=(2, 3, 4), dtype=torch.float32).to(part.device)  # [bs, Q, G]
+            if wsum is None:  # CPU stand-in: the weight sums of this rank's cameras
+                wsum = wts.sum(dim=(2, 3, 4), dtype=torch.float32).to(part.device)  # [bs, Q, G]
+            # one all-reduce of [bs*Q, C + G]: numerators and weight sums together
             buf = torch.cat([part.reshape(bs * q_n, c_n), wsum.reshape(bs * q_n, g_n)], dim=1)
         else:
             buf = part.reshape(bs * q_n, c_n)
         if self.world > 1:
             dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
-        out = buf[:, :c_n].reshape(bs, q_n, c_n)
-        if normalize:
-            ws = buf[:, c_n:].reshape(bs, q_n, g_n)
-            if bool((ws == 0).any()):
-                raise ValueError("an anchor's weights sum to zero, cannot renormalize")
-            out = (out.reshape(bs, q_n, g_n, c_n // g_n) / ws.unsqueeze(-1)).reshape(bs, q_n, c_n)
-        return out
+        if not normalize:
+            return buf.reshape(bs, q_n, c_n)
+        out = buf[:, :c_n].contiguous()
+        ws = buf[:, c_n:].contiguous()
+        if self.normalize_fn is not None:
+            return self.normalize_fn(out, ws).reshape(bs, q_n, c_n)
+        if bool((ws == 0).any()):
+            raise ValueError("an anchor's weights sum to zero, cannot renormalize")
+        return (out.reshape(bs, q_n, g_n, c_n // g_n) / ws.reshape(bs, q_n, g_n, 1)).reshape(bs, q_n, c_n)
 
     @classmethod
     def for_device_features(cls, n_cams, local_feats, precision="fast", group=None):
@@ -87,10 +95,9 @@ class CameraShardedAggregation:
         from . import ops
 
         def local(loc, wts):
-            return ops.deformable_aggregation(local_feats, None, None, loc, wts, precision=precision,
-                                              normalize=False)
+            return ops.deformable_aggregation_partial(local_feats, loc, wts, precision=precision)
 
-        return cls(n_cams, local, group)
+        return cls(n_cams, local, group, ops.normalize_groups)
 
 
 def init_from_env(backend: str | None = None):

@@ -225,6 +225,46 @@ class Cameras:
         return cls(K, R, t, device)
 
 
+def deformable_aggregation_partial(feats: DeviceFeatures, sampling_location, weights, precision="fast"):
+    """Un-normalised FAST aggregation of ``feats``' cameras plus the
+    per-(query, group) weight sums: the partials a camera-sharded rank
+    all-reduces (C ABI ``msda_dense_partial``).  Returns (out [bs, Q, C],
+    weight_sums [bs, Q, G])."""
+    dev = feats.table.device
+    loc = sampling_location.to(device=dev, dtype=torch.float32).contiguous()
+    wts = weights.to(device=dev, dtype=torch.float32).contiguous()
+    bs, q_n, p_n = int(loc.shape[0]), int(loc.shape[1]), int(loc.shape[2])
+    g_n = int(wts.shape[-1])
+    if tuple(loc.shape) != (bs, q_n, p_n, feats.n_cams, 2) or tuple(wts.shape) != (
+            bs, q_n, p_n, feats.n_cams, feats.n_levels, g_n):
+        raise ValueError("sampling_location [bs, Q, P, cams, 2] and weights [bs, Q, P, cams, L, G] expected")
+    out = torch.empty((bs, q_n, feats.channels), dtype=torch.float32, device=dev)
+    wsum = torch.empty((bs, q_n, g_n), dtype=torch.float32, device=dev)
+    lib = L.lib()
+    ws = WORKSPACE.get(dev, lib.msda_dense_workspace_size(bs, q_n, p_n, feats.n_cams, feats.n_levels, g_n,
+                                                          feats.channels))
+    fd = feats.descriptor()
+    code = lib.msda_dense_partial(ctypes.byref(fd), q_n, p_n, g_n, _ptr(loc), _ptr(wts), precision_code(precision),
+                                  _ptr(out), _ptr(wsum), _ptr(ws), ws.numel(), _stream(dev))
+    if code != L.MSDA_OK:
+        raise_for_status(code, -1, "deformable_aggregation_partial")
+    return out, wsum
+
+
+def normalize_groups(out, weight_sums, check=True):
+    """In place: out[..., c] /= weight_sums[..., c // (C / G)] (C ABI
+    ``msda_dense_normalize``); a zero sum raises the reference's ValueError."""
+    dev = out.device
+    c_n, g_n = int(out.shape[-1]), int(weight_sums.shape[-1])
+    n_q = out.numel() // c_n
+    if not out.is_contiguous() or not weight_sums.is_contiguous() or weight_sums.numel() != n_q * g_n:
+        raise ValueError("contiguous out [..., C] and weight_sums [..., G] expected")
+    ws = WORKSPACE.get(dev, 256)
+    code = L.lib().msda_dense_normalize(_ptr(out), _ptr(weight_sums), n_q, c_n, g_n, _ptr(ws), _stream(dev))
+    _check_call(code, ws, dev, check, "normalize_groups")
+    return out
+
+
 def msda_dense_project(feats: DeviceFeatures, anchors, learned_offsets, cameras: Cameras, strides, weights, dt=0.0,
                        precision="fast", normalize=False, out=None, check=False):
     """Dense MSDA with keypoint generation + projection fused into the kernel.

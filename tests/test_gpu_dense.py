@@ -330,3 +330,31 @@ def test_dense_exact_one_pass_with_ties(cuda_dev, dt, groups, normalize):
                                      check=True).cpu().numpy()
     ref = mo.msda_dense_groups(seen, tiles, shape, loc, wts, 4, normalize=normalize)
     assert out.tobytes() == ref.tobytes()
+
+
+def test_camera_sharded_partials_on_device(cuda_dev):
+    """The camera-sharded driver's device path (single rank: no all-reduce):
+    msda_dense_partial numerators + weight sums, then msda_dense_normalize —
+    equals the normalised one-call aggregation; zero sums raise."""
+    import torch
+
+    from paper_2601_10819_b200 import ops
+    from paper_2601_10819_b200.dist import CameraShardedAggregation
+
+    rng = np.random.default_rng(29)
+    grids, shape, loc, wts = helpers.make_dense(rng, bs=2, n_q=10, n_p=13, cams=4, n_levels=4, groups=8,
+                                                channels=256, size_lo=6, size_hi=24)
+    feats, table, tiles = _feats(ops, torch, grids, shape, cuda_dev, batch=2)
+    t = lambda a: torch.from_numpy(a).to(cuda_dev)  # noqa: E731
+    part, wsum = ops.deformable_aggregation_partial(feats, t(loc), t(wts))
+    assert np.allclose(wsum.cpu().numpy(), wts.sum(axis=(2, 3, 4)), rtol=1e-5)
+    agg = CameraShardedAggregation.for_device_features(4, feats)
+    out = agg(t(loc), t(wts), normalize=True).cpu().numpy()
+    ref = mo.msda_dense_groups(table, tiles, shape, loc, wts, 4, normalize=True)
+    assert rel(out, ref) <= 1e-4
+    raw = agg(t(loc), t(wts), normalize=False).cpu().numpy()
+    assert rel(raw, mo.msda_dense_groups(table, tiles, shape, loc, wts, 4, normalize=False)) <= 1e-4
+    zero = wts.copy()
+    zero[1, 3, :, :, :, 2] = 0.0
+    with pytest.raises(ValueError, match="sum to zero"):
+        agg(t(loc), t(zero), normalize=True)
