@@ -16,8 +16,7 @@
 //
 // One thread per pair, 16 x 16 pairs per CTA (8 x 8 above D ~ 800); the
 // CTA's query and detection embedding rows are staged in shared memory (rows
-// padded by one double so the detection rows a warp reads sit in different
-// banks).
+// padded to an even pitch with a 16-B bank skew; read two doubles at a time).
 #include <algorithm>
 
 #include "msda_common.cuh"
@@ -51,13 +50,25 @@ __device__ double pairwise_block(const double* a, const double* b, int n) {
     for (int i = 0; i < n; ++i) res = __dadd_rn(res, sqdiff(a, b, i));
     return res;
   }
-  double r[8];
+  // rows are 16-B aligned: two doubles per shared-memory load
+  auto sq8 = [&](int i0, double* v) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j) r[j] = sqdiff(a, b, j);
+    for (int j = 0; j < 8; j += 2) {
+      const double2 x = *reinterpret_cast<const double2*>(a + i0 + j);
+      const double2 y = *reinterpret_cast<const double2*>(b + i0 + j);
+      const double d0 = __dsub_rn(x.x, y.x), d1 = __dsub_rn(x.y, y.y);
+      v[j] = __dmul_rn(d0, d0);
+      v[j + 1] = __dmul_rn(d1, d1);
+    }
+  };
+  double r[8];
+  sq8(0, r);
   int i = 8;
   for (; i < n - (n % 8); i += 8) {
+    double t[8];
+    sq8(i, t);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], sqdiff(a, b, i + j));
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], t[j]);
   }
   double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                          __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
@@ -104,7 +115,7 @@ __device__ double pairwise_sum_sq(const double* a, const double* b, int n) {
 template <int kTile>
 __global__ void __launch_bounds__(kTile * kTile) assoc_cost_kernel(AssocArgs a) {
   extern __shared__ __align__(16) double sm[];
-  const int pitch = a.D + 1;
+  const int pitch = a.D + 2 + (a.D & 1);  // even (16-B aligned rows), 16 B of bank skew per row
   double* s_q = sm;
   double* s_d = sm + kTile * pitch;
   const int q0 = blockIdx.y * kTile, d0 = blockIdx.x * kTile;
@@ -150,7 +161,8 @@ int32_t msda_assoc_cost(const double* q_centers, const double* d_centers, const 
               alpha_emb, alpha_geo, cost,         solver_cost,  admissible};
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   // 16 x 16 pairs per CTA while both 16-row tiles fit in shared memory, else 8 x 8
-  const size_t smem16 = 2 * (size_t)16 * (dim + 1) * sizeof(double);
+  const int pitch = dim + 2 + (dim & 1);
+  const size_t smem16 = 2 * (size_t)16 * pitch * sizeof(double);
   if (smem16 <= 200 * 1024) {
     if (smem16 > 48 * 1024 && cudaFuncSetAttribute(assoc_cost_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    (int)smem16) != cudaSuccess)
@@ -158,7 +170,7 @@ int32_t msda_assoc_cost(const double* q_centers, const double* d_centers, const 
     const dim3 grid((unsigned)((n_d + 15) / 16), (unsigned)((n_q + 15) / 16));
     assoc_cost_kernel<16><<<grid, 256, smem16, s>>>(a);
   } else {
-    const size_t smem8 = 2 * (size_t)8 * (dim + 1) * sizeof(double);
+    const size_t smem8 = 2 * (size_t)8 * pitch * sizeof(double);
     if (cudaFuncSetAttribute(assoc_cost_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem8) !=
         cudaSuccess)
       return MSDA_CUDA_ERROR;

@@ -192,8 +192,8 @@ __device__ __forceinline__ void store4(void* out, int dtype, int64_t i, const fl
   }
 }
 
-// CTA = 64 cells of one (camera, level) grid.  Threads 0..63 run the depth
-// contest for one cell each; then every thread owns a fixed 4-channel chunk
+// CTA = 64 cells of one (camera, level) grid.  Four threads per cell run the
+// depth contest (a quarter of the entities each); then every thread owns a fixed 4-channel chunk
 // (C % 4 == 0) and walks the cells with stride blockDim / (C / 4).
 __global__ void __launch_bounds__(256) paint_kernel(PaintArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -207,14 +207,16 @@ __global__ void __launch_bounds__(256) paint_kernel(PaintArgs a) {
   for (int e = threadIdx.x; e < a.n_ent; e += blockDim.x) s_r[e] = a.rects[(int64_t)cam * a.n_ent + e];
   __syncthreads();
   const double stride = a.strides[level];
-  if (threadIdx.x < kPaintCells) {
-    const int cell = cell0 + threadIdx.x;
+  {  // depth contest: 4 threads per cell, each a quarter of the entities, then the
+     // lexicographic minimum (depth, entity index) == the first strictly-nearest
+    const int cl = threadIdx.x >> 2, part = threadIdx.x & 3;
+    const int cell = cell0 + cl;
     int win = -1;
+    double best = INFINITY;
     if (cell < H * W) {
       const int y = cell / W, x = cell - y * W;
       const double u = __dmul_rn((double)x + 0.5, stride), v = __dmul_rn((double)y + 0.5, stride);
-      double best = INFINITY;
-      for (int e = 0; e < a.n_ent; ++e) {
+      for (int e = part; e < a.n_ent; e += 4) {
         const Rect r = s_r[e];
         if (r.valid && r.u0 <= u && u <= r.u1 && r.v0 <= v && v <= r.v1 && r.depth < best) {
           best = r.depth;
@@ -222,7 +224,16 @@ __global__ void __launch_bounds__(256) paint_kernel(PaintArgs a) {
         }
       }
     }
-    s_win[threadIdx.x] = win < a.n_obj ? win : -1;  // occluders paint nothing
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int ow = __shfl_xor_sync(0xffffffffu, win, o);
+      if (ow >= 0 && (win < 0 || ob < best || (ob == best && ow < win))) {
+        best = ob;
+        win = ow;
+      }
+    }
+    if (part == 0) s_win[cl] = win < a.n_obj ? win : -1;  // occluders paint nothing
   }
   __syncthreads();
   const int n_cells = min(kPaintCells, H * W - cell0);
