@@ -241,52 +241,10 @@ __global__ void __launch_bounds__(kOaeWarps * 32, 2) oae_warp_kernel(OaeArgs a) 
     float2 acc[VEC / 2];
 #pragma unroll
     for (int e = 0; e < VEC / 2; ++e) acc[e] = make_float2(0.0f, 0.0f);
-    while (mask) {
-      const int p = __ffs(mask) - 1;
-      mask &= mask - 1;
-      float2 g[VEC / 2];  // level mean of the bilinear reads, two channels per FFMA2
-#pragma unroll
-      for (int e = 0; e < VEC / 2; ++e) g[e] = make_float2(0.0f, 0.0f);
-      for (int l0 = 0; l0 < a.L; l0 += LV) {
-        SampleRec r[LV];
-        Row<NV> c[LV][4];
-#pragma unroll
-        for (int j = 0; j < LV; ++j) {
-          const int l = l0 + j;
-          if (l < a.L) {
-            r[j] = s_rec[warp][p * a.L + l];
-          } else {
-            r[j].row[0] = r[j].row[1] = r[j].row[2] = r[j].row[3] = -1;
-          }
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (r[j].row[k] >= 0) c[j][k] = ld_row<NV>(feat + (size_t)r[j].row[k] * row_bytes);
-            else
-#pragma unroll
-              for (int i = 0; i < NV; ++i) c[j][k].v[i] = make_uint4(0, 0, 0, 0);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < LV; ++j) {
-          if (l0 + j >= a.L) break;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            float f[VEC];
-            raw_to_f32<T, VEC>(reinterpret_cast<const uint32_t*>(c[j][k].v), f);
-            const float cw = r[j].iw[k] * inv_l;
-            const float2 w2 = make_float2(cw, cw);
-#pragma unroll
-            for (int e = 0; e < VEC / 2; ++e) g[e] = __ffma2_rn(make_float2(f[2 * e], f[2 * e + 1]), w2, g[e]);
-          }
-        }
-      }
-      float2 dp = make_float2(0.0f, 0.0f);
-#pragma unroll
-      for (int e = 0; e < VEC / 2; ++e) dp = __ffma2_rn(g[e], d2[e], dp);
-      double dot = (double)dp.x + (double)dp.y;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-      const float sc = (float)dot * inv_sqrt_d;
+    // two keypoints per step: their row loads are in flight together and the
+    // two score reductions interleave; the softmax update stays in keypoint order
+    auto online = [&](const float2* g, float dotf) {
+      const float sc = dotf * inv_sqrt_d;
       const float m2 = fmaxf(m, sc);
       const float scale = expf(m - m2), w = expf(sc - m2);  // online softmax (oae.py:117-122)
       z = z * scale + w;
@@ -294,6 +252,72 @@ __global__ void __launch_bounds__(kOaeWarps * 32, 2) oae_warp_kernel(OaeArgs a) 
 #pragma unroll
       for (int e = 0; e < VEC / 2; ++e) acc[e] = __ffma2_rn(g[e], w2, __fmul2_rn(acc[e], s2));
       m = m2;
+    };
+    while (mask) {
+      const int pa = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const bool has_b = mask != 0;
+      const int pb = has_b ? __ffs(mask) - 1 : pa;
+      if (has_b) mask &= mask - 1;
+      float2 ga[VEC / 2], gb[VEC / 2];
+#pragma unroll
+      for (int e = 0; e < VEC / 2; ++e) ga[e] = gb[e] = make_float2(0.0f, 0.0f);
+      constexpr int LP = LV >= 2 ? LV / 2 : 1;  // levels per keypoint per load round
+      for (int l0 = 0; l0 < a.L; l0 += LP) {
+        SampleRec r[2][LP];
+        Row<NV> c[2][LP][4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+          for (int j = 0; j < LP; ++j) {
+            const int l = l0 + j;
+            const bool use = l < a.L && (h == 0 || has_b);
+            if (use) {
+              r[h][j] = s_rec[warp][(h ? pb : pa) * a.L + l];
+            } else {
+              r[h][j].row[0] = r[h][j].row[1] = r[h][j].row[2] = r[h][j].row[3] = -1;
+              r[h][j].iw[0] = r[h][j].iw[1] = r[h][j].iw[2] = r[h][j].iw[3] = 0.0f;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              if (r[h][j].row[k] >= 0) c[h][j][k] = ld_row<NV>(feat + (size_t)r[h][j].row[k] * row_bytes);
+              else
+#pragma unroll
+                for (int i = 0; i < NV; ++i) c[h][j][k].v[i] = make_uint4(0, 0, 0, 0);
+            }
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float2* g = h ? gb : ga;
+#pragma unroll
+          for (int j = 0; j < LP; ++j) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              float f[VEC];
+              raw_to_f32<T, VEC>(reinterpret_cast<const uint32_t*>(c[h][j][k].v), f);
+              const float cw = r[h][j].iw[k] * inv_l;
+              const float2 w2 = make_float2(cw, cw);
+#pragma unroll
+              for (int e = 0; e < VEC / 2; ++e) g[e] = __ffma2_rn(make_float2(f[2 * e], f[2 * e + 1]), w2, g[e]);
+            }
+          }
+        }
+      }
+      float2 da = make_float2(0.0f, 0.0f), db = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int e = 0; e < VEC / 2; ++e) {
+        da = __ffma2_rn(ga[e], d2[e], da);
+        db = __ffma2_rn(gb[e], d2[e], db);
+      }
+      float sa = da.x + da.y, sb = db.x + db.y;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {  // two warp all-reduces, interleaved
+        sa += __shfl_xor_sync(0xffffffffu, sa, o);
+        sb += __shfl_xor_sync(0xffffffffu, sb, o);
+      }
+      online(ga, sa);
+      if (has_b) online(gb, sb);
     }
     __syncwarp();  // the next camera restages s_rec
     const double vis = (double)a.vis[(int64_t)q * a.cams + cam];
