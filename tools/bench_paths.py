@@ -198,6 +198,42 @@ def oae_case(reps, dev, cams=32, C=256, Q=900):
             "queries_per_s": Q / (med / 1e3)}
 
 
+def frame_case(reps, dev, cams=64, C=256, G=8, Q=900, P=13, layers=6, precision="fast_h2"):
+    """The paper headline (BASELINE configs[2]): one frame of 64 fp16 camera
+    streams through 6 decoder layers of MSDA — 6 deformable_aggregation calls,
+    each with its own sampling locations and weights, captured once in a CUDA
+    graph and replayed (no host work between layers)."""
+    feats = make_feats(cams, CFG1_LEVELS, C, torch.float16, dev)
+    ins = []
+    for layer in range(layers):
+        g = torch.Generator(device=dev).manual_seed(100 + layer)
+        loc = torch.rand((1, Q, P, cams, 2), generator=g, device=dev)
+        w = torch.softmax(torch.randn((1, Q, P * cams * 4, G), generator=g, device=dev), dim=2)
+        ins.append((loc, w.reshape(1, Q, P, cams, 4, G).contiguous()))
+    outs = [torch.empty((1, Q, C), device=dev) for _ in range(layers)]
+
+    def frame():
+        for (loc, w), o in zip(ins, outs):
+            ops.deformable_aggregation(feats, None, None, loc, w, precision=precision, out=o)
+
+    frame()  # workspace allocation outside the capture
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        frame()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=s):
+            frame()
+    torch.cuda.current_stream().wait_stream(s)
+    med, best = time_fn(graph.replay, reps, flush=False)
+    return {"config": "cfg3-frame", "path": f"{layers} x deformable_aggregation in one CUDA graph",
+            "precision": precision, "dtype": "float16", "cams": cams, "layers": layers,
+            "frame_us": med * 1e3, "best_us": best * 1e3, "per_layer_us": med * 1e3 / layers,
+            "frames_per_s": 1e3 / med, "camera_streams_at_30fps": int(cams * (1e3 / med) / 30)}
+
+
 def paint_case(reps, dev, cams=64, C=256, n_obj=40, n_occ=8):
     """Feature painting of a cfg3-shaped scene (64 ring cameras, 704x256
     images, strides 4-32, C=256) straight into the f16 table, device
@@ -259,6 +295,8 @@ def main():
         "cfg5": lambda: dense_case("cfg5 512 cams fp16 (1 GPU)", 512, CFG1_LEVELS, 256, 8, torch.float16, "fast",
                                    max(5, args.reps // 4), dev),
         "project": lambda: project_case(args.reps, dev),
+        "frame": lambda: frame_case(max(5, args.reps // 2), dev),
+        "frame_fast": lambda: frame_case(max(5, args.reps // 2), dev, precision="fast"),
         "paint": lambda: paint_case(args.reps, dev),
         "assoc": lambda: assoc_case(args.reps, dev),
         "cfg4": lambda: oae_case(max(5, args.reps // 4), dev),
