@@ -222,6 +222,12 @@ int32_t msda_csr_host(msda_context_t *ctx, const void *const *level_data, const 
                       const int32_t *level, const float *u, const float *v, const float *weight,
                       int32_t precision, int32_t normalize, float *out, uint8_t *empty);
 
+/* Host->device bytes the last msda_csr_host call moved: whole grids copied
+ * plus, for large sparsely sampled grids in pinned (device-visible) host
+ * memory, only the corner rows the plan touches (fetched over PCIe by the
+ * device, once each).                                                       */
+long long msda_context_last_h2d_bytes(const msda_context_t *ctx);
+
 #ifdef __cplusplus
 }
 #endif

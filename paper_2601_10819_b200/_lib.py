@@ -74,6 +74,7 @@ SIGNATURES = {
     "msda_read_status": (I32, [P, P, ctypes.POINTER(I32), ctypes.POINTER(I64)]),
     "msda_context_create": (I32, [I32, ctypes.POINTER(P)]),
     "msda_context_destroy": (None, [P]),
+    "msda_context_last_h2d_bytes": (ctypes.c_longlong, [P]),
     "msda_csr_host": (I32, [P, P, P, I32, I32, I32, I32, I64, P, P, P, P, P, P, I32, I32, P, P]),
 }
 

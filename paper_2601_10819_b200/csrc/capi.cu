@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <new>
 #include <vector>
 
@@ -19,6 +20,63 @@ namespace {
 __global__ void f32_to_f16_kernel(const float* __restrict__ src, __half* __restrict__ dst, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = __float2half_rn(src[i]);
+}
+
+// ---- touched-row fetch for the host-buffer path ----
+// Large, sparsely sampled grids (the finest levels: at cfg2 a level-0 cell is
+// read 0.36 times per call) are not copied whole: when the caller's host
+// buffer is pinned (device-visible through UVA), one warp per plan sample
+// claims each in-grid corner row in a bitmap and copies only the rows no one
+// claimed before, straight from host memory over PCIe into the device table.
+// Same bilinear corner rule as the plan (make_record), so every row the
+// gather reads is present; the other rows are never read.
+struct FetchArgs {
+  const int32_t* cam;
+  const int32_t* lvl;
+  const float* u;
+  const float* v;
+  int64_t n_samples;
+  int32_t n_cams, n_levels;
+  const int32_t* shape;
+  const int64_t* start;
+  const unsigned long long* src;  // [n_tiles] device-visible host address of each fetched tile, 0 = copied whole
+  char* table;                    // device table
+  uint32_t* claimed;              // [rows / 32 + 1] bitmap, zeroed
+  unsigned long long* fetched;    // rows fetched (bytes = rows * row_bytes)
+  int32_t row_bytes;
+};
+
+__global__ void __launch_bounds__(256) fetch_rows_kernel(FetchArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t sidx = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); sidx < a.n_samples;
+       sidx += warps) {
+    const int c = a.cam[sidx], l = a.lvl[sidx];
+    if (c < 0 || c >= a.n_cams || l < 0 || l >= a.n_levels) continue;  // the plan kernel reports it
+    const int t = c * a.n_levels + l;
+    const unsigned long long src = a.src[t];
+    if (!src) continue;
+    const float uu = a.u[sidx], vv = a.v[sidx];
+    if (!(isfinite(uu) && isfinite(vv))) continue;
+    const SampleRec r = make_record(uu, vv, 0, a.shape[2 * t], a.shape[2 * t + 1]);  // tile-local rows
+    unsigned todo = 0;
+    if (lane < 4 && r.row[lane] >= 0) {
+      const int64_t g = a.start[t] + r.row[lane];
+      const uint32_t bit = 1u << (g & 31);
+      todo = (atomicOr(a.claimed + (g >> 5), bit) & bit) ? 0u : 1u;
+    }
+    unsigned mask = __ballot_sync(0xffffffffu, todo) & 0xfu;
+    while (mask) {
+      const int k = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const int32_t row = r.row[k];
+      const char* from = reinterpret_cast<const char*>(src) + (size_t)row * a.row_bytes;
+      char* to = a.table + (size_t)(a.start[t] + row) * a.row_bytes;
+      for (int off = lane * 16; off < a.row_bytes; off += 32 * 16)
+        *reinterpret_cast<uint4*>(to + off) = *reinterpret_cast<const uint4*>(from + off);
+      if (lane == 0) atomicAdd(a.fetched, 1ull);
+    }
+  }
 }
 
 cudaError_t launch_f32_to_f16(const float* src, __half* dst, int64_t n, cudaStream_t s) {
@@ -38,6 +96,15 @@ int num_sms_for_current_device() {
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   if (dev >= 0 && dev < 64) g_num_sms_cache[dev] = n;
   return n;
+}
+
+// MSDA_HOST_FETCH=0 copies every grid of the host-buffer path whole
+bool fetch_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("MSDA_HOST_FETCH");
+    return !(e && e[0] == '0');
+  }();
+  return v;
 }
 
 int32_t validate_features(const msda_features_t* f) {
@@ -136,7 +203,10 @@ struct msda_context {
   cudaStream_t stream = nullptr;
   void* arena = nullptr;
   size_t arena_bytes = 0;
+  long long last_h2d_bytes = 0;  // host->device bytes moved by the last msda_csr_host call
 };
+
+long long msda_context_last_h2d_bytes(const msda_context_t* ctx) { return ctx ? ctx->last_h2d_bytes : -1; }
 
 int32_t msda_context_create(int32_t device, msda_context_t** ctx) {
   if (!ctx) return MSDA_BAD_ARG;
@@ -201,13 +271,33 @@ int32_t msda_csr_host(msda_context_t* ctx, const void* const* level_data, const 
   const bool cvt_half = (precision == MSDA_EXACT_HALF && dtype == MSDA_F32);
   const int32_t dev_dtype = cvt_half ? MSDA_F16 : dtype;
   const size_t half_b = cvt_half ? align_up((size_t)rows * channels * 2, 256) : 0;
-  // arena: [workspace | table | shape | start | offsets | cam | lvl | u | v | w | out | empty]
+  // tiles fetched row by row instead of copied whole: pinned (device-visible)
+  // host buffers of grids with more cells than 4 corners x the mean samples
+  // per tile, i.e. where most rows are never read (MSDA_HOST_FETCH=0: copy all)
+  std::vector<unsigned long long> src(n_tiles, 0ull);
+  const int64_t per_tile = n_tiles > 0 ? S / n_tiles : 0;
+  const bool fetch_ok = !cvt_half && fetch_enabled() && (channels * esz) % 16 == 0;
+  for (int t = 0; t < n_tiles && fetch_ok; ++t) {
+    const int64_t cells = (int64_t)spatial_shape[2 * t] * spatial_shape[2 * t + 1];
+    if (cells <= 4 * per_tile || !level_data[t]) continue;
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, level_data[t]) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (pa.type == cudaMemoryTypeHost && pa.devicePointer && reinterpret_cast<uintptr_t>(pa.devicePointer) % 16 == 0)
+      src[t] = reinterpret_cast<unsigned long long>(pa.devicePointer);
+  }
+  bool any_fetch = false;
+  for (int t = 0; t < n_tiles; ++t) any_fetch |= src[t] != 0;
+  // arena: [workspace | table | shape | start | offsets | cam | lvl | u | v | w | out | empty | src | bitmap | count]
+  const size_t src_b = align_up((size_t)n_tiles * 8, 256), bm_b = align_up((size_t)(rows / 32 + 1) * 4, 256);
   const size_t ws_b = align_up(msda_csr_workspace_size(n_queries, S, channels), 256);
   const size_t tab_b = align_up((size_t)rows * channels * esz, 256);
   const size_t shp_b = align_up((size_t)n_tiles * 2 * 4, 256), st_b = align_up((size_t)n_tiles * 8, 256);
   const size_t off_b = align_up((size_t)(n_queries + 1) * 8, 256), i_b = align_up((size_t)S * 4, 256);
   const size_t out_b = align_up((size_t)n_queries * channels * 4, 256), emp_b = align_up((size_t)n_queries, 256);
-  const size_t total = ws_b + tab_b + half_b + shp_b + st_b + off_b + 5 * i_b + out_b + emp_b;
+  const size_t total = ws_b + tab_b + half_b + shp_b + st_b + off_b + 5 * i_b + out_b + emp_b + src_b + bm_b + 256;
   int32_t st = ctx_reserve(ctx, total);
   if (st != MSDA_OK) return st;
   char* p = reinterpret_cast<char*>(ctx->arena);
@@ -223,13 +313,20 @@ int32_t msda_csr_host(msda_context_t* ctx, const void* const* level_data, const 
   float* d_v = reinterpret_cast<float*>(p); p += i_b;
   float* d_w = reinterpret_cast<float*>(p); p += i_b;
   float* d_out = reinterpret_cast<float*>(p); p += out_b;
-  uint8_t* d_emp = reinterpret_cast<uint8_t*>(p);
+  uint8_t* d_emp = reinterpret_cast<uint8_t*>(p); p += emp_b;
+  unsigned long long* d_src = reinterpret_cast<unsigned long long*>(p); p += src_b;
+  uint32_t* d_bm = reinterpret_cast<uint32_t*>(p); p += bm_b;
+  unsigned long long* d_fetched = reinterpret_cast<unsigned long long*>(p);
   cudaStream_t s = ctx->stream;
   bool ok = true;
-  for (int t = 0; t < n_tiles && ok; ++t)
-    ok = cudaMemcpyAsync(d_tab + (size_t)start[t] * channels * esz, level_data[t],
-                         (size_t)spatial_shape[2 * t] * spatial_shape[2 * t + 1] * channels * esz,
-                         cudaMemcpyHostToDevice, s) == cudaSuccess;
+  long long h2d = 0;
+  for (int t = 0; t < n_tiles && ok; ++t) {
+    if (src[t]) continue;  // fetched row by row below
+    const size_t nb = (size_t)spatial_shape[2 * t] * spatial_shape[2 * t + 1] * channels * esz;
+    ok = cudaMemcpyAsync(d_tab + (size_t)start[t] * channels * esz, level_data[t], nb, cudaMemcpyHostToDevice, s) ==
+         cudaSuccess;
+    h2d += (long long)nb;
+  }
   ok = ok && cudaMemcpyAsync(d_shape, spatial_shape, (size_t)n_tiles * 8, cudaMemcpyHostToDevice, s) == cudaSuccess;
   ok = ok && cudaMemcpyAsync(d_start, start.data(), (size_t)n_tiles * 8, cudaMemcpyHostToDevice, s) == cudaSuccess;
   ok = ok && cudaMemcpyAsync(d_off, offsets, (size_t)(n_queries + 1) * 8, cudaMemcpyHostToDevice, s) == cudaSuccess;
@@ -241,6 +338,17 @@ int32_t msda_csr_host(msda_context_t* ctx, const void* const* level_data, const 
     ok = ok && cudaMemcpyAsync(d_w, weight, S * 4, cudaMemcpyHostToDevice, s) == cudaSuccess;
   }
   if (!ok) return MSDA_CUDA_ERROR;
+  h2d += (long long)(n_tiles * 16 + (n_queries + 1) * 8 + S * 20);
+  if (any_fetch) {
+    ok = cudaMemcpyAsync(d_src, src.data(), (size_t)n_tiles * 8, cudaMemcpyHostToDevice, s) == cudaSuccess &&
+         cudaMemsetAsync(d_bm, 0, bm_b + 256, s) == cudaSuccess;  // bitmap + counter
+    if (!ok) return MSDA_CUDA_ERROR;
+    FetchArgs fa{d_cam, d_lvl, d_u, d_v, S, n_cams, n_levels, d_shape, d_start, d_src, d_tab, d_bm, d_fetched,
+                 (int32_t)(channels * esz)};
+    const int64_t blocks = std::min<int64_t>((S + 7) / 8, (int64_t)num_sms_for_current_device() * 16);
+    if (blocks > 0) fetch_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(fa);
+    if (cudaGetLastError() != cudaSuccess) return MSDA_CUDA_ERROR;
+  }
   if (cvt_half) {
     if (launch_f32_to_f16(reinterpret_cast<const float*>(d_tab), reinterpret_cast<__half*>(d_half),
                           rows * (int64_t)channels, s) != cudaSuccess)
@@ -265,8 +373,14 @@ int32_t msda_csr_host(msda_context_t* ctx, const void* const* level_data, const 
     return MSDA_CUDA_ERROR;
   int32_t dev_status = 0;
   int64_t detail = 0;
-  st = msda_read_status(d_ws, s, &dev_status, &detail);
+  st = msda_read_status(d_ws, s, &dev_status, &detail);  // synchronises the stream
   if (st != MSDA_OK) return st;
+  if (any_fetch) {
+    unsigned long long rows_fetched = 0;
+    if (cudaMemcpy(&rows_fetched, d_fetched, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return MSDA_CUDA_ERROR;
+    h2d += (long long)(rows_fetched * channels * esz);
+  }
+  ctx->last_h2d_bytes = h2d;
   return dev_status;
 }
 

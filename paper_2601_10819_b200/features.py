@@ -179,6 +179,13 @@ class _Contexts:
 _CONTEXTS = _Contexts()
 
 
+def last_h2d_bytes(device: int = 0) -> int:
+    """Host->device bytes moved by the last host-buffer call on ``device``:
+    whole grids copied plus the corner rows fetched from large, sparsely
+    sampled grids in pinned host memory (C ABI msda_context_last_h2d_bytes)."""
+    return int(L.lib().msda_context_last_h2d_bytes(_CONTEXTS.get(device)))
+
+
 def _pyramid_map(pyramids) -> dict:
     out = {}
     for pyr in pyramids:

@@ -258,3 +258,31 @@ def test_fast_csr_skips_canonicalisation(c_oracle, cuda_dev, dt, channels, norma
     zero[int(offsets[3]):int(offsets[4])] = 0.0
     with pytest.raises(ValueError, match="sum to zero"):
         ops.msda_csr(feats, *args[:5], t(zero), precision="fast")
+
+
+def test_host_path_fetches_sparse_grids_from_pinned_memory(c_oracle, cuda_dev):
+    """msda_optimized with pyramids in pinned host memory: the finest grids
+    (more cells than 4 x the mean samples per grid) are not copied whole —
+    only the corner rows the plan touches cross PCIe — and the bytes still
+    equal the oracle's; pageable grids are copied whole."""
+    import torch
+
+    from paper_2601_10819_b200 import features as F
+    from paper_2601_10819_b200.workload import BenchWorkload, generate_workload
+
+    wl = BenchWorkload(cameras=4, levels=4, channels=64, queries=120, points_per_query=13, level0_size=(90, 160))
+    host = torch.empty((wl.num_rows, wl.channels), dtype=torch.float32, pin_memory=True)
+    gw = generate_workload(wl, table_out=host.numpy())
+    pyrs, plan = _gw_pyramids(F, gw)
+    out, empty = F.msda_optimized(pyrs, plan)
+    moved = F.last_h2d_bytes()
+    ref, _ = c_oracle.msda_c(gw.table, gw.tiles, wl.levels, gw.offsets, gw.camera_ids, gw.levels, gw.us, gw.vs,
+                             gw.weights)
+    assert out.tobytes() == ref.tobytes()
+    table_bytes = gw.table.nbytes
+    assert moved < 0.6 * table_bytes  # level 0 (90 x 160 cells, ~1.5 k samples) fetched row by row
+    paged = [F.FeaturePyramid(p.camera_id, [F.FeatureGrid(stride=g.stride, values=np.array(g.values))
+                                            for g in p.levels]) for p in pyrs]
+    out2, _ = F.msda_optimized(paged, plan)
+    assert out2.tobytes() == ref.tobytes()
+    assert F.last_h2d_bytes() >= table_bytes

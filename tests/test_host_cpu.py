@@ -16,7 +16,7 @@ ROOT = Path(__file__).resolve().parent.parent
 def _declared_symbols():
     hdr = (ROOT / "include" / "msda_b200.h").read_text()
     hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
-    return sorted(set(re.findall(r"\b(msda_[a-z_]+)\s*\(", hdr)))
+    return sorted(set(re.findall(r"\b(msda_[a-z0-9_]+)\s*\(", hdr)))
 
 
 def test_library_exports_every_declared_symbol():
