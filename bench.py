@@ -400,8 +400,8 @@ def run_ours(args, cfg, rank, local_rank, world):
         "e2e": {"value": world * wl.cameras / e2e_s, "unit": "camera-frames/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
                 "api": "paper_2601_10819_b200.features.msda_optimized -> C-ABI msda_csr_host (pinned host buffers)",
-                "transfer": "grids copied whole, except grids with more cells than 4 x the mean samples per grid "
-                            "(level 0 here): only their touched corner rows cross PCIe, fetched once each by the "
+                "transfer": "grids copied whole, except grids with more cells than 2 x the mean samples per grid "
+                            "(levels 0-1 here): only their touched corner rows cross PCIe, fetched once each by the "
                             "device from the pinned buffer",
                 "table_bytes": int(table_bytes),
                 "bitwise_equal_to_device_path": same},
