@@ -160,9 +160,18 @@ class SamplePlan:
 
 
 class _Contexts:
+    """One C-ABI host context (device arena + stream) per device.  A context
+    is not re-entrant, so calls on it are serialised by a per-device lock
+    (the reference allows concurrent calls from worker threads)."""
+
     def __init__(self):
         self._lock = threading.Lock()
         self._ctx = {}
+        self._call_locks = {}
+
+    def call_lock(self, device: int):
+        with self._lock:
+            return self._call_locks.setdefault(device, threading.Lock())
 
     def get(self, device: int):
         with self._lock:
@@ -255,10 +264,11 @@ def _run(pyramids, plan: SamplePlan, precision_code: int, normalize: bool, devic
     out = np.empty((q_n, channels), dtype=np.float32)
     empty = np.empty(q_n, dtype=np.uint8)
     cam_idx = np.ascontiguousarray(cam_idx, dtype=np.int32)
-    code = L.lib().msda_csr_host(
-        _CONTEXTS.get(device), ptrs, _ptr(shape), len(ids), n_levels, channels, L.MSDA_F32, q_n,
-        _ptr(plan.offsets), _ptr(cam_idx), _ptr(plan.levels), _ptr(plan.us), _ptr(plan.vs), _ptr(plan.weights),
-        precision_code, int(bool(normalize)), _ptr(out), _ptr(empty))
+    with _CONTEXTS.call_lock(device):
+        code = L.lib().msda_csr_host(
+            _CONTEXTS.get(device), ptrs, _ptr(shape), len(ids), n_levels, channels, L.MSDA_F32, q_n,
+            _ptr(plan.offsets), _ptr(cam_idx), _ptr(plan.levels), _ptr(plan.us), _ptr(plan.vs),
+            _ptr(plan.weights), precision_code, int(bool(normalize)), _ptr(out), _ptr(empty))
     del keep
     raise_for_status(code, -1, "msda")
     return out, empty.astype(bool)
