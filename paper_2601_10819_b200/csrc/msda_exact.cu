@@ -34,6 +34,7 @@
 //   gather_exact_kernel register-pipelined fallback for channel slices that do
 //                       not span whole warps (small C in tests / odd groups).
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <type_traits>
 
@@ -691,12 +692,14 @@ template <typename T, int VEC, bool HALF, int D, bool RAW, int GW = 1>
 cudaError_t launch_gather_pipe(const GatherArgs& g, cudaStream_t stream) {
   constexpr int BYTES = VEC * (int)sizeof(T);
   const int smem = kPipeWarps * PipeSmem<BYTES, D, GW>::kPerWarp;
-  static bool attr_set = false;  // per instantiation; idempotent
-  if (!attr_set) {
+  static std::atomic<bool> attr_set[64];  // per instantiation and device (function attributes are per device)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr_set[dev].load(std::memory_order_acquire)) {
     cudaError_t e = cudaFuncSetAttribute(gather_pipe_kernel<T, VEC, HALF, D, RAW, GW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    if (dev >= 0 && dev < 64) attr_set[dev].store(true, std::memory_order_release);
   }
   const int64_t warps = g.n_queries * (g.C / VEC / 32);
   const int64_t grid = (warps + kPipeWarps - 1) / kPipeWarps;
