@@ -178,7 +178,8 @@ int32_t msda_csr_stages(const msda_features_t* feat, const msda_csr_plan_t* plan
   if ((stage_mask & 1) &&
       launch_plan_canon(*feat, *plan, normalize, w, num_sms_for_current_device(), stream) != cudaSuccess)
     return MSDA_CUDA_ERROR;
-  if ((stage_mask & 2) && launch_gather_exact(*feat, *plan, prec, w, out, empty, stream) != cudaSuccess)
+  if ((stage_mask & 2) &&
+      launch_gather_exact(*feat, *plan, prec, w, out, empty, stream, 0, 0, -1, 1, normalize) != cudaSuccess)
     return MSDA_CUDA_ERROR;
   return MSDA_OK;
 }

@@ -710,7 +710,8 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
       if (cudaGetLastError() != cudaSuccess) return MSDA_CUDA_ERROR;
       ExactWorkspace ew1 = ew;
       ew1.wn = wn_g;
-      const cudaError_t e = launch_gather_exact(*f, plan1, precision, ew1, out, nullptr, s, 0, 0, -1, G);
+      // weights arrive normalised per group (dense_canon_kernel): no division in the gather
+      const cudaError_t e = launch_gather_exact(*f, plan1, precision, ew1, out, nullptr, s, 0, 0, -1, G, 0);
       if (e == cudaSuccess) return MSDA_OK;
       if (e != cudaErrorNotSupported) return MSDA_CUDA_ERROR;
     }
@@ -737,7 +738,7 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
       dense_expand_kernel<false><<<(unsigned)nq, 256, 0, s>>>(a, g, d_off, d_cam, d_lvl, d_u, d_v, d_w);
     if (cudaGetLastError() != cudaSuccess) return MSDA_CUDA_ERROR;
     if (launch_plan_canon(*f, plan, normalize, ew, sms, s, Q) != cudaSuccess) return MSDA_CUDA_ERROR;
-    if (launch_gather_exact(*f, plan, precision, ew, out, nullptr, s, g * cpg, cpg) != cudaSuccess)
+    if (launch_gather_exact(*f, plan, precision, ew, out, nullptr, s, g * cpg, cpg, -1, 1, normalize) != cudaSuccess)
       return MSDA_CUDA_ERROR;
   }
   return MSDA_OK;

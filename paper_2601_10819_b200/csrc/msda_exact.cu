@@ -66,7 +66,8 @@ struct PlanArgs {
   int64_t queries_per_batch;  // query q reads batch q / queries_per_batch ...
   int64_t rows_per_batch;     // ... whose table starts rows_per_batch rows later
   SampleRec* rec;
-  float* wn;
+  float* wn;    // [S] raw weights in canonical order (the gather divides by qsum)
+  float* qsum;  // [n_queries] sequential f32 weight sum per query (normalize)
   u64* g_hi;  // global scratch [S] for queries longer than kPlanSmemCap
   u64* g_lo;
   int32_t* g_idx;
@@ -255,32 +256,71 @@ __device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_
       }
     }
     __syncthreads();
-    canon_slots(n, n_tiles, khi, klo, sdst, sw, s_run);
-    // thread 0 runs the sequential f32 weight sum (features.py:264-269) while
-    // the other threads write the records, which do not depend on it
     const int64_t row_base = (q / a.queries_per_batch) * a.rows_per_batch;
-    if (threadIdx.x == 0) {
-      float ws = 0.0f;
-      if (a.normalize) {
-        ws = sequential_sum(sw, n, SMEM);
-        if (ws == 0.0f) set_status(a.status, MSDA_ZERO_WEIGHT_SUM, q);
-      }
-      *s_wsum = ws;
-    } else {
-      for (int i = threadIdx.x - 1; i < n; i += blockDim.x - 1) {
-        const u64 kt = khi[i], kp = klo[i];
-        const int t = (int)(kt >> 32);
-        const float vv = unord_f32((uint32_t)(kp >> 32));
-        const float uu = unord_f32((uint32_t)(kp & 0xffffffffu));
-        const int tt = t < n_tiles ? t : 0;
-        a.rec[lo + sdst[i]] = make_record(uu, vv, row_base + a.start[tt], a.shape[2 * tt], a.shape[2 * tt + 1]);
+    // record + raw weight of the key at canonical slot `slot`
+    auto emit = [&](u64 kt, u64 kp, int slot) {
+      const int t = (int)(kt >> 32);
+      const float vv = unord_f32((uint32_t)(kp >> 32));
+      const float uu = unord_f32((uint32_t)(kp & 0xffffffffu));
+      const int tt = t < n_tiles ? t : 0;
+      a.rec[lo + slot] = make_record(uu, vv, row_base + a.start[tt], a.shape[2 * tt], a.shape[2 * tt + 1]);
+      a.wn[lo + slot] = key_weight(kt);
+      sw[slot] = key_weight(kt);
+    };
+    // grouped by (camera, level)?  run heads / tails record their run in the same pass
+    bool bad = false;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint32_t t = (uint32_t)(khi[i] >> 32);
+      const uint32_t tp = i > 0 ? (uint32_t)(khi[i - 1] >> 32) : 0xffffffffu;
+      const uint32_t tn = i + 1 < n ? (uint32_t)(khi[i + 1] >> 32) : 0xffffffffu;
+      bad |= i > 0 && t < tp;
+      if (t < (uint32_t)kRunTable) {
+        if (t != tp) s_run[2 * t] = (int16_t)i;
+        if (t != tn) s_run[2 * t + 1] = (int16_t)(i + 1);
       }
     }
-    __syncthreads();
-    const float wsum = *s_wsum;
-    for (int i = threadIdx.x; i < n; i += blockDim.x)  // canonical slot order: coalesced
-      a.wn[lo + i] = a.normalize ? __fdiv_rn(sw[i], wsum) : sw[i];
-    __syncthreads();
+    bool rank_path = !__syncthreads_or(bad) && n_tiles <= kRunTable && n <= 32767;
+    if (rank_path) {  // canonical slot = run start + rank of (v, u) in the run
+      bool long_run = false;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const u64 it = khi[i], ip = klo[i];
+        const uint32_t t = (uint32_t)(it >> 32);
+        const int rs = s_run[2 * t], re = s_run[2 * t + 1];
+        if (re - rs > kRunCap) {  // quadratic ranks would be too slow: sort instead
+          long_run = true;
+          continue;
+        }
+        int rank = 0;
+        bool tie = false;
+#pragma unroll 4
+        for (int j = rs; j < re; ++j) {  // branch-free: one 64-bit (v, u) compare per run member
+          const u64 jp = klo[j];
+          rank += jp < ip ? 1 : 0;
+          tie |= (jp == ip) & (j != i);
+        }
+        if (tie) {  // exact (v, u) tie (rare): weight, then position
+          const uint32_t wi = (uint32_t)it;
+          for (int j = rs; j < re; ++j) {
+            if (j == i || klo[j] != ip) continue;
+            const uint32_t wj = (uint32_t)khi[j];
+            rank += (wj < wi || (wj == wi && j < i)) ? 1 : 0;
+          }
+        }
+        emit(it, ip, rs + rank);
+      }
+      rank_path = !__syncthreads_or(long_run);
+    }
+    if (!rank_path) {  // ungrouped or long runs: full bitonic sort, slots = sorted order
+      bitonic_sort_canon(khi, klo, n);
+      for (int i = threadIdx.x; i < n; i += blockDim.x) emit(khi[i], klo[i], i);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0 && a.normalize) {  // sequential f32 sum in canonical order (features.py:264-269)
+      const float ws = sequential_sum(sw, n, SMEM);
+      if (ws == 0.0f) set_status(a.status, MSDA_ZERO_WEIGHT_SUM, q);
+      a.qsum[q] = ws;
+    }
+    __syncthreads();  // shared memory is reused by the next query
   }
 }
 
@@ -297,6 +337,7 @@ struct GatherArgs {
   const int64_t* offsets;
   const SampleRec* rec;
   const float* wn;
+  const float* qsum;  // per-query weight sums of the canonical plan (wn holds raw weights), or null
   float* out;
   uint8_t* empty;
   float2 one2;  // (1, 1)   — FFMA2 operands that make exact adds / products;
@@ -398,6 +439,7 @@ __global__ void __launch_bounds__(256) gather_exact_kernel(GatherArgs a) {
       if (i + j < hi) {
         r[j] = ld_rec(a.rec + i + j);
         s[j] = __ldg(a.wn + i + j);
+        if (a.qsum && a.normalize) s[j] = __fdiv_rn(s[j], a.qsum[q]);
       } else {
         r[j].row[0] = r[j].row[1] = r[j].row[2] = r[j].row[3] = -1;
         r[j].iw[0] = r[j].iw[1] = r[j].iw[2] = r[j].iw[3] = 0.0f;
@@ -522,6 +564,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   const uint32_t row_bytes = (uint32_t)a.row_elems * (uint32_t)sizeof(T);
 
   const bool head = c0 == lane * VEC;  // the query's first channel-slice warp reports plan errors
+  const float wq = (!RAW && a.qsum && a.normalize && n > 0) ? a.qsum[q] : 1.0f;
   float wsum = 1.0f;
   if constexpr (RAW) {
     if (a.normalize) {  // per-query weight sum, any order (FAST)
@@ -562,6 +605,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
         r = ld_rec(rec + s);
         if constexpr (GW == 1) {
           r_wn = __ldg(wnp + s);
+          if (a.qsum && a.normalize) r_wn = __fdiv_rn(r_wn, wq);  // w / sum (features.py:271-273)
         } else {
 #pragma unroll
           for (int k = 0; k < GW; ++k)
@@ -750,12 +794,12 @@ cudaError_t reset_exact_workspace(const ExactWorkspace& w, cudaStream_t stream) 
 }
 
 size_t exact_workspace_bytes(int64_t n_queries, int64_t n_samples) {
-  (void)n_queries;
   size_t b = kStatusBytes;
   b += align_up((size_t)n_samples * sizeof(SampleRec), 256);
   b += align_up((size_t)n_samples * sizeof(float), 256);
   b += 2 * align_up((size_t)n_samples * sizeof(u64), 256);
   b += align_up((size_t)n_samples * sizeof(int32_t), 256);
+  b += align_up((size_t)n_queries * sizeof(float), 256);  // per-query weight sums
   return b;
 }
 
@@ -773,6 +817,8 @@ ExactWorkspace carve_exact_workspace(void* ws, int64_t n_samples) {
   w.g_lo = reinterpret_cast<u64*>(p);
   p += align_up((size_t)n_samples * sizeof(u64), 256);
   w.g_idx = reinterpret_cast<int32_t*>(p);
+  p += align_up((size_t)n_samples * sizeof(int32_t), 256);
+  w.qsum = reinterpret_cast<float*>(p);
   return w;
 }
 
@@ -800,6 +846,7 @@ cudaError_t launch_plan_canon(const msda_features_t& f, const msda_csr_plan_t& p
   a.g_hi = w.g_hi;
   a.g_lo = w.g_lo;
   a.g_idx = w.g_idx;
+  a.qsum = w.qsum;
   a.status = w.status;
   // one CTA per query while they all fit on the device at once
   const int64_t grid = std::min<int64_t>(p.n_queries, (int64_t)num_sms * 8);
@@ -809,7 +856,7 @@ cudaError_t launch_plan_canon(const msda_features_t& f, const msda_csr_plan_t& p
 
 cudaError_t launch_gather_exact(const msda_features_t& f, const msda_csr_plan_t& p, int precision,
                                 const ExactWorkspace& w, float* out, uint8_t* empty, cudaStream_t stream,
-                                int c_off, int c_count, int fast_normalize, int n_groups) {
+                                int c_off, int c_count, int fast_normalize, int n_groups, int normalize) {
   const bool raw = fast_normalize >= 0;  // FAST on the raw plan (no canonicalisation pass)
   GatherArgs g{};
   g.n_groups = n_groups;
@@ -827,6 +874,7 @@ cudaError_t launch_gather_exact(const msda_features_t& f, const msda_csr_plan_t&
   g.offsets = p.offsets;
   g.rec = w.rec;
   g.wn = w.wn;
+  g.qsum = n_groups > 1 ? nullptr : w.qsum;
   g.out = out;
   g.empty = empty;
   g.one2 = make_float2(1.0f, 1.0f);
@@ -840,7 +888,7 @@ cudaError_t launch_gather_exact(const msda_features_t& f, const msda_csr_plan_t&
   g.start = f.scale_start_index;
   g.n_cams = f.n_cams;
   g.n_levels = f.n_levels;
-  g.normalize = raw ? fast_normalize : 0;
+  g.normalize = raw ? fast_normalize : normalize;
   g.status = w.status;
   const size_t esz = f.dtype == MSDA_F32 ? 4 : 2;
   // vector width must divide the slice and keep every row (and output) access aligned

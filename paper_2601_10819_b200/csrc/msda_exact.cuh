@@ -11,6 +11,7 @@ struct ExactWorkspace {
   unsigned long long* g_hi;
   unsigned long long* g_lo;
   int32_t* g_idx;
+  float* qsum;  // [n_queries] per-query weight sums written by the plan
 };
 
 size_t exact_workspace_bytes(int64_t n_queries, int64_t n_samples);
@@ -21,7 +22,8 @@ cudaError_t launch_plan_canon(const msda_features_t& f, const msda_csr_plan_t& p
                               int64_t queries_per_batch = 0);
 cudaError_t launch_gather_exact(const msda_features_t& f, const msda_csr_plan_t& p, int precision,
                                 const ExactWorkspace& w, float* out, uint8_t* empty, cudaStream_t stream,
-                                int c_off = 0, int c_count = 0, int fast_normalize = -1, int n_groups = 1);
+                                int c_off = 0, int c_count = 0, int fast_normalize = -1, int n_groups = 1,
+                                int normalize = 1);
 // FAST on the CSR plan: one gather launch straight from the raw plan arrays
 // (fast_normalize = normalize flag); cudaErrorNotSupported when the channel
 // slice does not span whole warps (the caller then runs the exact stages).
