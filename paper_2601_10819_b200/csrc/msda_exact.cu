@@ -8,15 +8,18 @@
 //                       of features.py:261-263.  When the query arrives grouped
 //                       by (camera, level) — the reference bench generator and
 //                       every dense expansion do — each sample's canonical
-//                       slot is its run start (a shared-memory table) plus its
-//                       rank in the run (one 64-bit (v, u) compare per run
-//                       member); otherwise a bitonic sort.  Then the sequential
-//                       f32 weight sum in canonical order (features.py:264-269)
-//                       and one 32-B SampleRec + normalised weight per sample,
-//                       scattered to its canonical slot.
+//                       slot is its run start (a shared-memory table built in
+//                       the same pass that checks the grouping) plus its rank
+//                       in the run (one 64-bit (v, u) compare per run member),
+//                       and its 32-B SampleRec and raw weight are written there
+//                       in that pass; otherwise a bitonic sort.  Then the
+//                       sequential f32 weight sum in canonical order
+//                       (features.py:264-269), one float per query.
 //
 //   gather_pipe_kernel  one warp per (query, 32*VEC channels): walks the
-//                       query's records in canonical order.  Corner rows
+//                       query's records in canonical order (its batch loader
+//                       turns each raw weight into w / sum, features.py:271-
+//                       273).  Corner rows
 //                       (channel-last, 16-B per lane, whole 32-B sectors) are
 //                       prefetched D samples ahead with cp.async (LDGSTS,
 //                       zero-fill for out-of-grid corners) into a per-warp
@@ -116,61 +119,6 @@ __device__ void bitonic_sort_canon(u64* kt, u64* kp, int n) {
   }
 }
 
-// Canonicalise one query's n keys.  On return sdst[i] = canonical slot of key
-// i and sw[slot] = its weight; keys are untouched (rank path) or sorted in
-// place with sdst[i] = i.  s_run holds [start, end) of each tile's run.
-__device__ void canon_slots(int n, int n_tiles, u64* kt, u64* kp, int32_t* sdst, float* sw, int16_t* s_run) {
-  bool bad = false;
-  for (int i = threadIdx.x + 1; i < n; i += blockDim.x) bad |= (kt[i] >> 32) < (kt[i - 1] >> 32);
-  bool rank_path = !__syncthreads_or(bad) && n_tiles <= kRunTable && n <= 32767;
-  if (rank_path) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {  // run heads and tails record their run
-      const uint32_t t = (uint32_t)(kt[i] >> 32);
-      if (i == 0 || (uint32_t)(kt[i - 1] >> 32) != t) s_run[2 * t] = (int16_t)i;
-      if (i == n - 1 || (uint32_t)(kt[i + 1] >> 32) != t) s_run[2 * t + 1] = (int16_t)(i + 1);
-    }
-    __syncthreads();
-    bool long_run = false;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const uint32_t t = (uint32_t)(kt[i] >> 32);
-      long_run |= (s_run[2 * t + 1] - s_run[2 * t]) > kRunCap;
-    }
-    rank_path = !__syncthreads_or(long_run);
-  }
-  if (rank_path) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const u64 it = kt[i], ip = kp[i];
-      const uint32_t t = (uint32_t)(it >> 32);
-      const int rs = s_run[2 * t], re = s_run[2 * t + 1];
-      int rank = 0;
-      bool tie = false;
-#pragma unroll 4
-      for (int j = rs; j < re; ++j) {  // branch-free: one 64-bit (v, u) compare per run member
-        const u64 jp = kp[j];
-        rank += jp < ip ? 1 : 0;
-        tie |= (jp == ip) & (j != i);
-      }
-      if (tie) {  // exact (v, u) tie (rare): weight, then position
-        const uint32_t wi = (uint32_t)it;
-        for (int j = rs; j < re; ++j) {
-          if (j == i || kp[j] != ip) continue;
-          const uint32_t wj = (uint32_t)kt[j];
-          rank += (wj < wi || (wj == wi && j < i)) ? 1 : 0;
-        }
-      }
-      sdst[i] = rs + rank;
-      sw[rs + rank] = key_weight(it);
-    }
-  } else {
-    bitonic_sort_canon(kt, kp, n);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      sdst[i] = i;
-      sw[i] = key_weight(kt[i]);
-    }
-  }
-  __syncthreads();
-}
-
 // sequential float32 sum in canonical order (features.py:264-267): one
 // thread, loads issued well ahead of the dependent add chain
 __device__ __forceinline__ float sequential_sum(const float* sw, int n, bool vec_ok) {
@@ -196,15 +144,13 @@ __device__ __forceinline__ float sequential_sum(const float* sw, int n, bool vec
 
 template <bool SMEM>
 __device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_t lo, int n, int n_tiles, u64* khi,
-                                            u64* klo, float* sw, int32_t* sdst, int16_t* s_run, float* s_wsum);
+                                            u64* klo, float* sw, int16_t* s_run);
 
 __global__ void __launch_bounds__(kPlanThreads) plan_canon_kernel(PlanArgs a) {
   __shared__ __align__(16) u64 s_hi[kPlanSmemCap];
   __shared__ __align__(16) u64 s_lo[kPlanSmemCap];
   __shared__ __align__(16) float s_w[kPlanSmemCap];
-  __shared__ __align__(16) int32_t s_dst[kPlanSmemCap];
   __shared__ int16_t s_run[2 * kRunTable];
-  __shared__ float s_wsum;
   const int n_tiles = a.n_cams * a.n_levels;
 
   for (int64_t q = blockIdx.x; q < a.n_queries; q += gridDim.x) {
@@ -214,15 +160,15 @@ __global__ void __launch_bounds__(kPlanThreads) plan_canon_kernel(PlanArgs a) {
     // two inlined copies so the shared-memory one compiles to LDS/STS (a
     // pointer chosen at run time between smem and global would be generic)
     if (n <= kPlanSmemCap)
-      canon_query<true>(a, q, lo, n, n_tiles, s_hi, s_lo, s_w, s_dst, s_run, &s_wsum);
+      canon_query<true>(a, q, lo, n, n_tiles, s_hi, s_lo, s_w, s_run);
     else  // long query: global scratch (the wn slots double as its weight scratch)
-      canon_query<false>(a, q, lo, n, n_tiles, a.g_hi + lo, a.g_lo + lo, a.wn + lo, a.g_idx + lo, s_run, &s_wsum);
+      canon_query<false>(a, q, lo, n, n_tiles, a.g_hi + lo, a.g_lo + lo, a.wn + lo, s_run);
   }
 }
 
 template <bool SMEM>
 __device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_t lo, int n, int n_tiles, u64* khi,
-                                            u64* klo, float* sw, int32_t* sdst, int16_t* s_run, float* s_wsum) {
+                                            u64* klo, float* sw, int16_t* s_run) {
   {
     constexpr int U = 4;  // samples per thread whose loads are in flight together
     for (int i0 = threadIdx.x; i0 < n; i0 += U * blockDim.x) {
