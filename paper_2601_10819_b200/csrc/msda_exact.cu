@@ -550,8 +550,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
       } else {
         r = ld_rec(rec + s);
         if constexpr (GW == 1) {
-          r_wn = __ldg(wnp + s);
-          if (a.qsum && a.normalize) r_wn = __fdiv_rn(r_wn, wq);  // w / sum (features.py:271-273)
+          r_wn = __ldg(wnp + s);  // raw weight: divided when the batch is published (no load-use stall here)
         } else {
 #pragma unroll
           for (int k = 0; k < GW; ++k)
@@ -566,7 +565,8 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
     s_rows[buf * 32 + lane] = r_rows;
     s_iw[buf * 32 + lane] = r_iw;
     if constexpr (GW == 1) {
-      s_wn[buf * 32 + lane] = r_wn;
+      // w / sum (features.py:271-273); RAW batches arrive already divided
+      s_wn[buf * 32 + lane] = (!RAW && a.qsum && a.normalize) ? __fdiv_rn(r_wn, wq) : r_wn;
     } else {
 #pragma unroll
       for (int k = 0; k < GW; ++k) s_wn[(buf * 32 + lane) * GW + k] = r_wg[k];
