@@ -762,6 +762,7 @@ int32_t msda_dense(const msda_features_t* feat, int32_t n_queries, int32_t n_poi
   int32_t st = validate_dense(feat, n_queries, n_points, n_groups);
   if (st != MSDA_OK) return st;
   if (precision < MSDA_EXACT || precision > MSDA_FAST_H2) return MSDA_BAD_PRECISION;
+  if (n_queries == 0) return MSDA_OK;  // nothing to aggregate (empty tensors may carry null pointers)
   if (!sampling_location || !weights || !out || !workspace) return MSDA_BAD_ARG;
   return run_dense(feat, n_queries, n_points, n_groups, sampling_location, weights, precision, normalize, out,
                    workspace, workspace_bytes, reinterpret_cast<cudaStream_t>(stream), false, nullptr, 0, nullptr,
@@ -774,6 +775,7 @@ int32_t msda_dense_partial(const msda_features_t* feat, int32_t n_queries, int32
   int32_t st = validate_dense(feat, n_queries, n_points, n_groups);
   if (st != MSDA_OK) return st;
   if (precision != MSDA_FAST && precision != MSDA_FAST_H2) return MSDA_BAD_PRECISION;
+  if (n_queries == 0) return MSDA_OK;
   if (!sampling_location || !weights || !out || !weight_sums || !workspace) return MSDA_BAD_ARG;
   return run_dense(feat, n_queries, n_points, n_groups, sampling_location, weights, precision, 0, out, workspace,
                    workspace_bytes, reinterpret_cast<cudaStream_t>(stream), false, nullptr, 0, nullptr, nullptr,
@@ -804,6 +806,7 @@ int32_t msda_dense_project(const msda_features_t* feat, int32_t n_queries, const
   if (st != MSDA_OK) return st;
   if (precision < MSDA_EXACT || precision > MSDA_FAST_H2) return MSDA_BAD_PRECISION;
   if (n_learned < 0 || P > kMaxPoints || (n_learned > 0 && !learned_offsets)) return MSDA_BAD_ARG;
+  if (n_queries == 0) return MSDA_OK;
   if (!anchors || !cams || !cams->K || !cams->R || !cams->t || !strides || !weights || !out || !workspace)
     return MSDA_BAD_ARG;
   return run_dense(feat, n_queries, P, n_groups, nullptr, weights, precision, normalize, out, workspace,

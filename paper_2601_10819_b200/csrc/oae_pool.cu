@@ -410,6 +410,7 @@ int32_t msda_oae_pool(const msda_features_t* f, int32_t n_queries, const float* 
   if (f->n_cams <= 0 || f->n_levels <= 0 || f->channels <= 0 || n_queries < 0 || n_learned < 0) return MSDA_BAD_ARG;
   if (f->channels % 2) return MSDA_ODD_CHANNELS;
   if (f->channels > kOaeMaxC || 7 + n_learned > kOaeMaxPoints) return MSDA_BAD_ARG;
+  if (n_queries == 0) return MSDA_OK;  // empty tensors may carry null pointers
   if (!anchors || !cams || !cams->K || !cams->R || !cams->t || !strides || !descriptors || !visibility ||
       !memory || !out || !all_occluded || !workspace || workspace_bytes < kStatusBytes)
     return MSDA_BAD_ARG;
