@@ -236,13 +236,28 @@ __device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_
           long_run = true;
           continue;
         }
+        // v first: one 32-bit compare per run member (the high words of the
+        // (v, u) keys); members with the same v (rare for float
+        // coordinates) send the sample to the full (v, u, weight, position)
+        // comparison
+        const uint32_t* kv = reinterpret_cast<const uint32_t*>(klo) + 1;  // kv[2 j] = ord(v) of key j
+        const uint32_t iv = (uint32_t)(ip >> 32);
         int rank = 0;
-        bool tie = false;
+        bool same_v = false;
 #pragma unroll 4
-        for (int j = rs; j < re; ++j) {  // branch-free: one 64-bit (v, u) compare per run member
-          const u64 jp = klo[j];
-          rank += jp < ip ? 1 : 0;
-          tie |= (jp == ip) & (j != i);
+        for (int j = rs; j < re; ++j) {
+          const uint32_t jv = kv[2 * j];
+          rank += jv < iv ? 1 : 0;
+          same_v |= (jv == iv) & (j != i);
+        }
+        bool tie = false;
+        if (same_v) {  // redo with the 64-bit (v, u) keys
+          rank = 0;
+          for (int j = rs; j < re; ++j) {
+            const u64 jp = klo[j];
+            rank += jp < ip ? 1 : 0;
+            tie |= (jp == ip) & (j != i);
+          }
         }
         if (tie) {  // exact (v, u) tie (rare): weight, then position
           const uint32_t wi = (uint32_t)it;
