@@ -152,6 +152,9 @@ __global__ void __launch_bounds__(kPlanThreads) plan_canon_kernel(PlanArgs a) {
   __shared__ __align__(16) float s_w[kPlanSmemCap];
   __shared__ int16_t s_run[2 * kRunTable];
   const int n_tiles = a.n_cams * a.n_levels;
+  // programmatic dependent launch: the gather grid may be scheduled now; it
+  // waits (griddepcontrol.wait) for this grid's completion and memory flush
+  asm volatile("griddepcontrol.launch_dependents;");
 
   for (int64_t q = blockIdx.x; q < a.n_queries; q += gridDim.x) {
     const int64_t lo = a.offsets[q], hi = a.offsets[q + 1];
@@ -503,6 +506,10 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   constexpr int BYTES = VEC * (int)sizeof(T);
   using SM = PipeSmem<BYTES, D, GW>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  // launched programmatically after the canonicaliser: its records, weights
+  // and sums are visible once the primary grid has completed (a no-op when
+  // launched normally)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* base = smem_raw + warp * SM::kPerWarp;
   int4* s_rows = reinterpret_cast<int4*>(base + SM::kCorner);
@@ -709,8 +716,20 @@ cudaError_t launch_gather_pipe(const GatherArgs& g, cudaStream_t stream) {
   const int64_t warps = g.n_queries * (g.C / VEC / 32);
   const int64_t grid = (warps + kPipeWarps - 1) / kPipeWarps;
   if (grid == 0) return cudaSuccess;
-  gather_pipe_kernel<T, VEC, HALF, D, RAW, GW><<<(unsigned)grid, kPipeWarps * 32, smem, stream>>>(g);
-  return cudaGetLastError();
+  // programmatic stream serialisation: the launch overlaps the tail of the
+  // preceding canonicaliser (which triggers early); correctness rests on the
+  // kernel's griddepcontrol.wait
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kPipeWarps * 32);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gather_pipe_kernel<T, VEC, HALF, D, RAW, GW>, g);
 }
 
 template <typename T, int VEC, bool HALF>
