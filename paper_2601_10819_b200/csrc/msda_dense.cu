@@ -508,6 +508,7 @@ __global__ void __launch_bounds__(128) dense_canon_kernel(DenseArgs a, SampleRec
   const int G = a.G;
   const int64_t row_base = (int64_t)b * a.n_rows;
   unsigned char* s_valid = reinterpret_cast<unsigned char*>(s_kp + n);
+  asm volatile("griddepcontrol.launch_dependents;");  // the gather may launch early (it waits for completion)
   if constexpr (PROJECT) {
     anchor_keypoints(a, bq, s_kpt, a.status);
     __syncthreads();
