@@ -202,6 +202,8 @@ int32_t msda_read_status(const void* workspace, void* stream_, int32_t* status, 
 struct msda_context {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // whole-grid copies, concurrent with the row fetch on `stream`
+  cudaEvent_t fork = nullptr, join = nullptr;
   void* arena = nullptr;
   size_t arena_bytes = 0;
   long long last_h2d_bytes = 0;  // host->device bytes moved by the last msda_csr_host call
@@ -215,8 +217,11 @@ int32_t msda_context_create(int32_t device, msda_context_t** ctx) {
   if (!c) return MSDA_BAD_ARG;
   c->device = device;
   if (cudaSetDevice(device) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
-    delete c;
+      cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming) != cudaSuccess) {
+    msda_context_destroy(c);
     return MSDA_CUDA_ERROR;
   }
   *ctx = c;
@@ -228,6 +233,9 @@ void msda_context_destroy(msda_context_t* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->arena) cudaFree(ctx->arena);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->fork) cudaEventDestroy(ctx->fork);
+  if (ctx->join) cudaEventDestroy(ctx->join);
   delete ctx;
 }
 
@@ -235,6 +243,7 @@ static int32_t ctx_reserve(msda_context_t* ctx, size_t bytes) {
   if (bytes <= ctx->arena_bytes) return MSDA_OK;
   if (ctx->arena) {
     cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->copy_stream);
     cudaFree(ctx->arena);
     ctx->arena = nullptr;
     ctx->arena_bytes = 0;
@@ -322,13 +331,22 @@ int32_t msda_csr_host(msda_context_t* ctx, const void* const* level_data, const 
   cudaStream_t s = ctx->stream;
   bool ok = true;
   long long h2d = 0;
+  // Whole grids go by copy engine on the copy stream while the fetch kernel
+  // pulls the sparse grids' touched rows on `stream`: PCIe carries both at
+  // once (measured 53.4 GB/s together vs 55.6 copy-engine-only / 51.5
+  // zero-copy-only, profiles/r1/pcie_ceiling.txt).  The plan inputs go first
+  // on `stream` since the fetch needs them.
+  ok = cudaEventRecord(ctx->fork, s) == cudaSuccess && cudaStreamWaitEvent(ctx->copy_stream, ctx->fork, 0) ==
+       cudaSuccess;
   for (int t = 0; t < n_tiles && ok; ++t) {
     if (src[t]) continue;  // fetched row by row below
     const size_t nb = (size_t)spatial_shape[2 * t] * spatial_shape[2 * t + 1] * channels * esz;
-    ok = cudaMemcpyAsync(d_tab + (size_t)start[t] * channels * esz, level_data[t], nb, cudaMemcpyHostToDevice, s) ==
-         cudaSuccess;
+    if (nb == 0) continue;
+    ok = cudaMemcpyAsync(d_tab + (size_t)start[t] * channels * esz, level_data[t], nb, cudaMemcpyHostToDevice,
+                         ctx->copy_stream) == cudaSuccess;
     h2d += (long long)nb;
   }
+  ok = ok && cudaEventRecord(ctx->join, ctx->copy_stream) == cudaSuccess;
   ok = ok && cudaMemcpyAsync(d_shape, spatial_shape, (size_t)n_tiles * 8, cudaMemcpyHostToDevice, s) == cudaSuccess;
   ok = ok && cudaMemcpyAsync(d_start, start.data(), (size_t)n_tiles * 8, cudaMemcpyHostToDevice, s) == cudaSuccess;
   ok = ok && cudaMemcpyAsync(d_off, offsets, (size_t)(n_queries + 1) * 8, cudaMemcpyHostToDevice, s) == cudaSuccess;
@@ -339,17 +357,24 @@ int32_t msda_csr_host(msda_context_t* ctx, const void* const* level_data, const 
     ok = ok && cudaMemcpyAsync(d_v, v, S * 4, cudaMemcpyHostToDevice, s) == cudaSuccess;
     ok = ok && cudaMemcpyAsync(d_w, weight, S * 4, cudaMemcpyHostToDevice, s) == cudaSuccess;
   }
-  if (!ok) return MSDA_CUDA_ERROR;
+  if (!ok) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    return MSDA_CUDA_ERROR;
+  }
   h2d += (long long)(n_tiles * 16 + (n_queries + 1) * 8 + S * 20);
   if (any_fetch) {
     ok = cudaMemcpyAsync(d_src, src.data(), (size_t)n_tiles * 8, cudaMemcpyHostToDevice, s) == cudaSuccess &&
          cudaMemsetAsync(d_bm, 0, bm_b + 256, s) == cudaSuccess;  // bitmap + counter
-    if (!ok) return MSDA_CUDA_ERROR;
     FetchArgs fa{d_cam, d_lvl, d_u, d_v, S, n_cams, n_levels, d_shape, d_start, d_src, d_tab, d_bm, d_fetched,
                  (int32_t)(channels * esz)};
     const int64_t blocks = std::min<int64_t>((S + 7) / 8, (int64_t)num_sms_for_current_device() * 16);
-    if (blocks > 0) fetch_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(fa);
-    if (cudaGetLastError() != cudaSuccess) return MSDA_CUDA_ERROR;
+    if (ok && blocks > 0) fetch_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(fa);
+    ok = ok && cudaGetLastError() == cudaSuccess;
+  }
+  ok = ok && cudaStreamWaitEvent(s, ctx->join, 0) == cudaSuccess;
+  if (!ok) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    return MSDA_CUDA_ERROR;
   }
   if (cvt_half) {
     if (launch_f32_to_f16(reinterpret_cast<const float*>(d_tab), reinterpret_cast<__half*>(d_half),

@@ -208,35 +208,46 @@ def _ptr(a: np.ndarray):
     return ctypes.c_void_p(a.ctypes.data) if a.size else ctypes.c_void_p(0)
 
 
-def _prepare(pyr_map, plan: SamplePlan):
-    """Validation of features.py:222-238 + camera-id → dense index mapping."""
+def _prepare(pyr_map, plan: SamplePlan, defer_range_check: bool = False):
+    """Validation of features.py:222-238 + camera-id → dense index mapping.
+
+    ``defer_range_check``: with camera ids 0..n-1 and every pyramid at full
+    depth the device plan kernel range-checks every sample anyway (status
+    MSDA_BAD_TARGET); the host pass (~1 ms at 750 k samples, serial with the
+    transfer) then runs only to word the error the way the reference does."""
     ids = sorted(pyr_map)
     chans = {p.channels for p in pyr_map.values()}
     if len(chans) > 1:
         raise ValueError("all pyramids must share one channel count")
     n_levels = max(len(p.levels) for p in pyr_map.values())
     ragged = any(len(p.levels) != n_levels for p in pyr_map.values())
-    cam = plan.camera_ids
-    if ids == list(range(len(ids))):
+    cam, lv = plan.camera_ids, plan.levels
+    dense = ids == list(range(len(ids)))
+    deferred = defer_range_check and dense and not ragged
+    if dense:
         cam_idx = cam
-        if cam.size and (cam.min() < 0 or cam.max() >= len(ids)):
-            bad = cam[(cam < 0) | (cam >= len(ids))][0]
-            raise ValueError(f"plan references unknown camera id {bad}")
+        known = None
     else:
         id_arr = np.asarray(ids, dtype=np.int64)
         pos = np.searchsorted(id_arr, cam)
-        ok = (pos < len(ids)) & (id_arr[np.minimum(pos, len(ids) - 1)] == cam)
-        if not ok.all():
-            raise ValueError(f"plan references unknown camera id {cam[~ok][0]}")
-        cam_idx = pos.astype(np.int32)
-    lv = plan.levels
-    if lv.size:
-        if ragged:
-            nl = np.array([len(pyr_map[i].levels) for i in ids], dtype=np.int32)
-            if np.any((lv < 0) | (lv >= nl[cam_idx])):
-                raise ValueError("plan references a missing level of a camera")
-        elif lv.min() < 0 or lv.max() >= n_levels:
-            raise ValueError("plan references a missing level of a camera")
+        known = (pos < len(ids)) & (id_arr[np.minimum(pos, len(ids) - 1)] == cam)
+        cam_idx = np.where(known, pos, 0).astype(np.int32)
+    if cam.size and not deferred:
+        # _check_plan_targets (features.py:229-236) walks the sorted unique
+        # camera ids and raises at the first unknown id or the first camera
+        # with an out-of-range level: that is the smallest id among the bad samples
+        if known is None:
+            known = (cam >= 0) & (cam < len(ids))
+            idx = np.where(known, cam, 0)
+        else:
+            idx = cam_idx
+        nl = np.array([len(pyr_map[i].levels) for i in ids], dtype=np.int32)
+        bad = ~known | (lv < 0) | (lv >= nl[idx])
+        if bad.any():
+            c = cam[bad].min()
+            if int(c) not in pyr_map:
+                raise ValueError(f"plan references unknown camera id {c}")
+            raise ValueError(f"plan references a missing level of camera {c}")
     level_ptrs, shape, keep = [], [], []
     for i in ids:
         pyr = pyr_map[i]
@@ -260,7 +271,7 @@ def _run(pyramids, plan: SamplePlan, precision_code: int, normalize: bool, devic
         if plan.num_samples:
             raise ValueError(f"plan references unknown camera id {plan.camera_ids[0]}")
         return np.zeros((q_n, 0), dtype=np.float32), np.diff(plan.offsets) == 0
-    ids, n_levels, channels, cam_idx, ptrs, shape, keep = _prepare(pyr_map, plan)
+    ids, n_levels, channels, cam_idx, ptrs, shape, keep = _prepare(pyr_map, plan, defer_range_check=True)
     out = np.empty((q_n, channels), dtype=np.float32)
     empty = np.empty(q_n, dtype=np.uint8)
     cam_idx = np.ascontiguousarray(cam_idx, dtype=np.int32)
@@ -270,6 +281,8 @@ def _run(pyramids, plan: SamplePlan, precision_code: int, normalize: bool, devic
             _ptr(plan.offsets), _ptr(cam_idx), _ptr(plan.levels), _ptr(plan.us), _ptr(plan.vs),
             _ptr(plan.weights), precision_code, int(bool(normalize)), _ptr(out), _ptr(empty))
     del keep
+    if code != L.MSDA_OK:
+        _prepare(pyr_map, plan)  # a bad target outranks every other error, worded as the reference does
     raise_for_status(code, -1, "msda")
     return out, empty.astype(bool)
 

@@ -208,10 +208,18 @@ def test_errors_match_reference(cuda_dev):
     pyrs = _pyramids(F, grids, 1, 1)
     with pytest.raises(ValueError, match="sum to zero"):
         F.msda_optimized(pyrs, F.SamplePlan([[(0, 0, 1.0, 1.0, 0.0)]]))
-    with pytest.raises(ValueError):
+    with pytest.raises(ValueError, match="unknown camera id 5"):
         F.msda_optimized(pyrs, F.SamplePlan([[(5, 0, 1.0, 1.0, 1.0)]]))
-    with pytest.raises(ValueError):
+    with pytest.raises(ValueError, match="unknown camera id -1"):
+        F.msda_optimized(pyrs, F.SamplePlan([[(0, 0, 1.0, 1.0, 1.0)]] * 500 + [[(-1, 0, 1.0, 1.0, 1.0)]]))
+    with pytest.raises(ValueError, match="missing level of camera 0"):
         F.msda_optimized(pyrs, F.SamplePlan([[(0, 3, 1.0, 1.0, 1.0)]]))
+    # sorted-unique order: the smallest bad id is named (features.py:230)
+    with pytest.raises(ValueError, match="unknown camera id -1"):
+        F.msda_optimized(pyrs, F.SamplePlan([[(7, 0, 1.0, 1.0, 1.0)], [(-1, 0, 1.0, 1.0, 1.0)]]))
+    # the target check outranks the zero-sum check, as in the reference (features.py:231-238 before 268-269)
+    with pytest.raises(ValueError, match="unknown camera id 2"):
+        F.msda_optimized(pyrs, F.SamplePlan([[(0, 0, 1.0, 1.0, 0.0)], [(2, 0, 1.0, 1.0, 1.0)]]))
     with pytest.raises(ValueError):
         F.msda_optimized(pyrs + pyrs, F.SamplePlan([[(0, 0, 1.0, 1.0, 1.0)]]))
     with pytest.raises(ValueError):

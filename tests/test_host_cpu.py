@@ -83,6 +83,35 @@ def test_reference_mirror_validation():
     assert a.num_samples == 3 and list(a.query_indices()) == [0, 0, 2]
 
 
+def test_plan_target_errors_follow_reference_order():
+    """features.py:229-236: sorted unique camera ids, first unknown id or first
+    camera with an out-of-range level wins.  Host side only (no GPU call)."""
+    from paper_2601_10819_b200 import features as F
+
+    def pyr(cid, n_levels):
+        return F.FeaturePyramid(cid, [F.FeatureGrid(stride=8.0 * 2**m, values=np.zeros((2, 2, 2), np.float32))
+                                      for m in range(n_levels)])
+
+    def err(pyrs, per_query):
+        with pytest.raises(ValueError) as e:
+            F._prepare(F._pyramid_map(pyrs), F.SamplePlan(per_query))
+        return str(e.value)
+
+    dense = [pyr(0, 2), pyr(1, 2)]
+    assert err(dense, [[(7, 0, 1, 1, 1)], [(-1, 0, 1, 1, 1)]]) == "plan references unknown camera id -1"
+    assert err(dense, [[(1, 2, 1, 1, 1)], [(5, 0, 1, 1, 1)]]) == "plan references a missing level of camera 1"
+    assert err(dense, [[(5, 0, 1, 1, 1)], [(1, -1, 1, 1, 1)]]) == "plan references a missing level of camera 1"
+    sparse = [pyr(3, 1), pyr(9, 3)]
+    assert err(sparse, [[(9, 2, 1, 1, 1), (3, 1, 1, 1, 1)]]) == "plan references a missing level of camera 3"
+    assert err(sparse, [[(9, 3, 1, 1, 1), (4, 0, 1, 1, 1)]]) == "plan references unknown camera id 4"
+    ragged = [pyr(0, 1), pyr(1, 3)]
+    assert err(ragged, [[(1, 2, 1, 1, 1), (0, 1, 1, 1, 1)]]) == "plan references a missing level of camera 0"
+    F._prepare(F._pyramid_map(ragged), F.SamplePlan([[(1, 2, 1, 1, 1), (0, 0, 1, 1, 1)]]))
+    # deferred: dense ids at full depth leave the range check to the device status
+    F._prepare(F._pyramid_map(dense), F.SamplePlan([[(7, 0, 1, 1, 1)]]), defer_range_check=True)
+    assert err(ragged, [[(0, 1, 1, 1, 1)]]) == "plan references a missing level of camera 0"
+
+
 def test_product_never_imports_oracle():
     pkg = ROOT / "paper_2601_10819_b200"
     for py in pkg.rglob("*.py"):
