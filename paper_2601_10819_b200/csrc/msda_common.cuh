@@ -132,11 +132,9 @@ __device__ __forceinline__ void to_f32(const RawVec<VEC * sizeof(T)>& r, float* 
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < VEC / 2; ++i) {
-      __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
-      float2 f = __bfloat1622float2(h);
-      out[2 * i] = f.x;
-      out[2 * i + 1] = f.y;
+    for (int i = 0; i < VEC / 2; ++i) {  // bf16 -> f32 is a 16-bit shift
+      out[2 * i] = __uint_as_float(w[i] << 16);
+      out[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
     }
   }
 }

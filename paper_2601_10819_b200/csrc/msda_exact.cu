@@ -318,6 +318,16 @@ struct GatherArgs {
   DevStatus* status;
   // dense EXACT with channel groups: wn is [S, n_groups], channel c uses group c / cpg
   int32_t n_groups, cpg;
+  // DENSE (FAST on the Sparse4D layout): query q = (batch, anchor) owns the
+  // P x cams x L samples of loc [q, P, cams, 2] / w [q, P, cams, L, G]
+  const float* loc;
+  int32_t P;
+  int64_t q_per_batch, rows_per_batch;
+  float* wsum_out;  // [q, G] per-group weight sums, or null
+  // cameras split across warps: split k takes cameras [k cps, (k + 1) cps);
+  // with n_split > 1 the partial sums are red.add-ed into out / wsum_out
+  // (zeroed first) and normalised by a separate pass
+  int32_t cps, n_split;
 };
 
 __device__ __forceinline__ SampleRec ld_rec(const SampleRec* p) {
@@ -481,6 +491,7 @@ struct PipeSmem {
 };
 
 constexpr int kPipeWarps = 1;  // one warp per CTA: finest shared-memory granularity per SM
+constexpr int kDenseSplitSamples = 208;  // DENSE: target samples per warp (4 cameras of 4 levels x 13 points)
 
 // FAST: acc += (iw_k * wn) * c_k, fused, any order
 template <int VEC>
@@ -501,8 +512,21 @@ __device__ __forceinline__ void fast_accumulate(float* acc, const float (*c)[VEC
 // RAW = FAST on the CSR plan: records are built from the plan arrays in the
 // batch loader and the weight sum is a warp reduction (any order), so no
 // canonicalisation pass runs; the gather pipeline is the exact path's.
-template <typename T, int VEC, bool HALF, int D, bool RAW, int GW>
+//
+// DENSE = FAST on the Sparse4D layout (deformable_aggregation): records are
+// built from the anchor's normalised sampling locations (cell = loc * W - 0.5,
+// features.py:20-24) in camera-major, level, point order — every resident
+// anchor sweeps the cameras at about the same pace, so the live working set
+// is a few cameras' maps — and the lane's channel-group weight is summed on
+// the fly for the per-(anchor, group) normalisation at the end.
+// HACC (DENSE, f16 storage, FAST_H2): the paper's half2 accumulation — HFMA2
+// of the stored f16 pairs with half(iw_k * w_g) into a per-camera half2
+// partial, flushed into the f32 accumulator after every camera (runs of
+// L x P samples), as the warp-camera kernel does (msda_dense.cu).
+template <typename T, int VEC, bool HALF, int D, bool RAW, int GW, bool DENSE = false, bool HACC = false>
 __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs a) {
+  static_assert(!DENSE || (RAW && GW > 1), "DENSE builds raw records with per-group weights");
+  static_assert(!HACC || (DENSE && !HALF && std::is_same<T, __half>::value), "HACC: dense f16");
   constexpr int BYTES = VEC * (int)sizeof(T);
   using SM = PipeSmem<BYTES, D, GW>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -519,12 +543,22 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   const unsigned char* ring_ptr = base + lane * BYTES;
 
   const int warps_per_q = a.C / VEC / 32;
-  const int64_t gw = (int64_t)blockIdx.x * kPipeWarps + warp;
+  int64_t gw = (int64_t)blockIdx.x * kPipeWarps + warp;
+  int cam_lo = 0, n_cam = 0;
+  if constexpr (DENSE) {  // split-major: the first waves sweep the first cameras of every anchor
+    const int64_t per_split = a.n_queries * warps_per_q;
+    const int split = (int)(gw / per_split);
+    if (split >= a.n_split) return;
+    gw -= split * per_split;
+    cam_lo = split * a.cps;
+    n_cam = min(a.cps, a.n_cams - cam_lo);
+  }
   const int64_t q = gw / warps_per_q;
   if (q >= a.n_queries) return;
   const int c0 = (int)(gw - q * warps_per_q) * 32 * VEC + lane * VEC;
-  const int64_t lo = a.offsets[q];
-  const int n = (int)(a.offsets[q + 1] - lo);
+  const int nd = DENSE ? a.P * n_cam * a.n_levels : 0;  // samples of this dense split
+  const int64_t lo = DENSE ? 0 : a.offsets[q];
+  const int n = DENSE ? nd : (int)(a.offsets[q + 1] - lo);
   const SampleRec* rec = a.rec + lo;
   const float* wnp = a.wn + lo * (GW > 1 ? a.n_groups : 1);
   const int gl = GW > 1 ? (a.c_off + c0) / a.cpg : 0;  // this lane's channel group
@@ -534,7 +568,8 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   const bool head = c0 == lane * VEC;  // the query's first channel-slice warp reports plan errors
   const float wq = (!RAW && a.qsum && a.normalize && n > 0) ? a.qsum[q] : 1.0f;
   float wsum = 1.0f;
-  if constexpr (RAW) {
+  float wsum_g = 0.0f;  // DENSE: this lane's group weight sum
+  if constexpr (RAW && !DENSE) {
     if (a.normalize) {  // per-query weight sum, any order (FAST)
       float t = 0.0f;
       for (int s = lane; s < n; s += 32) t += __ldg(a.w + lo + s);
@@ -556,7 +591,23 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
     const int s = b * 32 + lane;
     if (s < n) {
       SampleRec r;
-      if constexpr (RAW) {
+      if constexpr (DENSE) {
+        const int per_cam = a.n_levels * a.P;
+        const int cs = s / per_cam, rem = s - cs * per_cam;
+        const int cam = cam_lo + cs;
+        const int l = rem / a.P, p = rem - l * a.P;
+        const int t = cam * a.n_levels + l;
+        const int H = a.shape[2 * t], W = a.shape[2 * t + 1];
+        const int64_t pc = (q * a.P + p) * a.n_cams + cam;
+        const float2 lp = __ldg(reinterpret_cast<const float2*>(a.loc) + pc);
+        const float uu = __fsub_rn(__fmul_rn(lp.x, (float)W), 0.5f);
+        const float vv = __fsub_rn(__fmul_rn(lp.y, (float)H), 0.5f);
+        r = make_record(uu, vv, (q / a.q_per_batch) * a.rows_per_batch + a.start[t], H, W);
+        const float* wp = a.w + (pc * a.n_levels + l) * a.n_groups;
+#pragma unroll
+        for (int k = 0; k < GW; ++k)
+          if (k < a.n_groups) r_wg[k] = __ldg(wp + k);
+      } else if constexpr (RAW) {
         const int64_t si = lo + s;
         int c = __ldg(a.cam + si), l = __ldg(a.lvl + si);
         const float uu = __ldg(a.u + si), vv = __ldg(a.v + si), ww = __ldg(a.w + si);
@@ -622,6 +673,31 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
 #pragma unroll
   for (int e = 0; e < VEC / 2; ++e) acch[e] = __float2half2_rn(0.0f);
 
+  __half2 hacc[HACC ? VEC / 2 : 1];
+#pragma unroll
+  for (int e = 0; e < (HACC ? VEC / 2 : 1); ++e) hacc[e] = __float2half2_rn(0.0f);
+  int run_left = HACC ? a.n_levels * a.P : 0;  // samples left in the current camera
+  auto hacc_sample = [&](const RawVec<BYTES>* cv, const float4 iw, const float wn) {
+    const float cw[4] = {iw.x * wn, iw.y * wn, iw.z * wn, iw.w * wn};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const __half2 cwh = __float2half2_rn(cw[k]);
+      const __half2* h = reinterpret_cast<const __half2*>(&cv[k]);
+#pragma unroll
+      for (int e = 0; e < VEC / 2; ++e) hacc[e] = __hfma2(h[e], cwh, hacc[e]);
+    }
+    if (--run_left == 0) {  // camera done: flush the half2 partial
+#pragma unroll
+      for (int e = 0; e < VEC / 2; ++e) {
+        const float2 f = __half22float2(hacc[e]);
+        accf[2 * e] += f.x;
+        accf[2 * e + 1] += f.y;
+        hacc[e] = __float2half2_rn(0.0f);
+      }
+      run_left = a.n_levels * a.P;
+    }
+  };
+
   // two samples per iteration: their shared-memory reads and products overlap;
   // the accumulation itself stays strictly sequential (i, then i + 1)
   static_assert(D >= 2, "ring depth");
@@ -639,7 +715,11 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
       cv0[k] = *reinterpret_cast<const RawVec<BYTES>*>(ring_ptr + read_off + k * 32 * BYTES);
       cv1[k] = *reinterpret_cast<const RawVec<BYTES>*>(ring_ptr + off1 + k * 32 * BYTES);
     }
-    if constexpr (!HALF) {
+    if constexpr (HACC) {
+      hacc_sample(cv0, iw0, wn0);
+      if (two) hacc_sample(cv1, iw1, wn1);
+      wsum_g += two ? wn0 + wn1 : wn0;
+    } else if constexpr (!HALF) {
       float c0[4][VEC], c1[4][VEC];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -649,6 +729,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
       if constexpr (RAW) {
         fast_accumulate<VEC>(accf, c0, iw0, wn0);
         if (two) fast_accumulate<VEC>(accf, c1, iw1, wn1);
+        if constexpr (DENSE) wsum_g += two ? wn0 + wn1 : wn0;
       } else {
         exact_accumulate<VEC>(accf, c0, iw0, wn0, a.one2, a.nz2);
         if (two) exact_accumulate<VEC>(accf, c1, iw1, wn1, a.one2, a.nz2);
@@ -680,6 +761,25 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   cp_async_wait<0>();
 
   float* o = a.out + q * a.out_stride + a.c_off + c0;
+  if constexpr (DENSE) {  // per-(anchor, group) renormalisation (FAST: sum in any order)
+    const bool ghead = (a.c_off + c0) % a.cpg == 0;  // the group's first lane reports
+    if (a.n_split > 1) {  // partial over a camera range: add into the zeroed totals
+      if (ghead && a.wsum_out) atomicAdd(a.wsum_out + q * a.n_groups + gl, wsum_g);
+      static_assert(VEC % 4 == 0, "float4 partials");
+#pragma unroll
+      for (int e = 0; e < VEC; e += 4)
+        atomicAdd(reinterpret_cast<float4*>(o + e), make_float4(accf[e], accf[e + 1], accf[e + 2], accf[e + 3]));
+      return;
+    }
+    if (ghead) {
+      if (a.wsum_out) a.wsum_out[q * a.n_groups + gl] = wsum_g;
+      if (a.normalize && wsum_g == 0.0f) set_status(a.status, MSDA_ZERO_WEIGHT_SUM, q);
+    }
+    if (a.normalize) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) accf[e] = accf[e] / wsum_g;
+    }
+  }
   if constexpr (!HALF) {
     if constexpr (VEC % 4 == 0) {
 #pragma unroll
@@ -700,7 +800,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   if (c0 == 0 && a.empty) a.empty[q] = (n == 0) ? 1 : 0;
 }
 
-template <typename T, int VEC, bool HALF, int D, bool RAW, int GW = 1>
+template <typename T, int VEC, bool HALF, int D, bool RAW, int GW = 1, bool DENSE = false, bool HACC = false>
 cudaError_t launch_gather_pipe(const GatherArgs& g, cudaStream_t stream) {
   constexpr int BYTES = VEC * (int)sizeof(T);
   const int smem = kPipeWarps * PipeSmem<BYTES, D, GW>::kPerWarp;
@@ -708,12 +808,12 @@ cudaError_t launch_gather_pipe(const GatherArgs& g, cudaStream_t stream) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || !attr_set[dev].load(std::memory_order_acquire)) {
-    cudaError_t e = cudaFuncSetAttribute(gather_pipe_kernel<T, VEC, HALF, D, RAW, GW>,
+    cudaError_t e = cudaFuncSetAttribute(gather_pipe_kernel<T, VEC, HALF, D, RAW, GW, DENSE, HACC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) attr_set[dev].store(true, std::memory_order_release);
   }
-  const int64_t warps = g.n_queries * (g.C / VEC / 32);
+  const int64_t warps = g.n_queries * (g.C / VEC / 32) * (DENSE ? g.n_split : 1);
   const int64_t grid = (warps + kPipeWarps - 1) / kPipeWarps;
   if (grid == 0) return cudaSuccess;
   // programmatic stream serialisation: the launch overlaps the tail of the
@@ -729,7 +829,7 @@ cudaError_t launch_gather_pipe(const GatherArgs& g, cudaStream_t stream) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gather_pipe_kernel<T, VEC, HALF, D, RAW, GW>, g);
+  return cudaLaunchKernelEx(&cfg, gather_pipe_kernel<T, VEC, HALF, D, RAW, GW, DENSE, HACC>, g);
 }
 
 template <typename T, int VEC, bool HALF>
@@ -768,6 +868,68 @@ int f32_lane_bytes() {
 }
 
 }  // namespace
+
+cudaError_t launch_gather_dense_fast(const msda_features_t& f, const DenseFastSpec& d, DevStatus* status, float* out,
+                                     cudaStream_t stream, bool* normalize_pending) {
+  *normalize_pending = false;
+  const int C = f.channels, G = d.G;
+  const size_t esz = f.dtype == MSDA_F32 ? 4 : 2;
+  if (G < 1 || G > 8 || C % G) return cudaErrorNotSupported;
+  const int cpg = C / G;
+  GatherArgs g{};
+  g.feat = f.data;
+  g.C = C;
+  g.row_elems = C;
+  g.c_off = 0;
+  g.out_stride = C;
+  g.n_queries = (int64_t)f.batch * d.Q;
+  g.out = out;
+  g.w = d.w;
+  g.loc = d.loc;
+  g.P = d.P;
+  g.q_per_batch = d.Q > 0 ? d.Q : 1;
+  g.rows_per_batch = f.n_rows;
+  g.wsum_out = d.wsum_out;
+  g.shape = f.spatial_shape;
+  g.start = f.scale_start_index;
+  g.n_cams = f.n_cams;
+  g.n_levels = f.n_levels;
+  g.normalize = d.normalize;
+  g.status = status;
+  g.n_groups = G;
+  g.cpg = cpg;
+  if (reinterpret_cast<uintptr_t>(f.data) % 16 || (C * esz) % 16 || reinterpret_cast<uintptr_t>(out) % 16 ||
+      reinterpret_cast<uintptr_t>(d.loc) % 8)
+    return cudaErrorNotSupported;
+  // a lane's channels must share one group, a query's channels span whole warps
+  const int vec = f.dtype == MSDA_F32 ? 4 : 8;  // 16-B lanes
+  if (C % (32 * vec) || cpg % vec) return cudaErrorNotSupported;
+  // cameras per warp: about kDenseSplitSamples samples per warp, so that
+  // short per-warp chains and many resident warps keep the gather fed
+  const int per_cam = d.P * f.n_levels;
+  const int want = std::max(1, (f.n_cams * per_cam + kDenseSplitSamples - 1) / kDenseSplitSamples);
+  g.cps = (f.n_cams + want - 1) / want;
+  g.n_split = (f.n_cams + g.cps - 1) / g.cps;
+  if (g.n_split > 1) {
+    if (!d.wsum_out && d.normalize && !d.wsum_scratch) return cudaErrorNotSupported;
+    if (!d.wsum_out && d.normalize) g.wsum_out = d.wsum_scratch;
+    if (cudaMemsetAsync(out, 0, (size_t)g.n_queries * C * 4, stream) != cudaSuccess) return cudaErrorUnknown;
+    if (g.wsum_out && cudaMemsetAsync(g.wsum_out, 0, (size_t)g.n_queries * G * 4, stream) != cudaSuccess)
+      return cudaErrorUnknown;
+    *normalize_pending = d.normalize != 0;
+  }
+  // ring depth 2: the dense gather is issue-bound (bf16/f16 -> f32 per
+  // channel-corner), so more resident warps (28 per SM at 8 KB of shared
+  // memory each) beat a deeper per-warp ring (D = 7: 12 per SM); measured at
+  // cfg1-cfg4, D in {2, 3, 4, 5, 7} x split in {104, 156, 208, 416} samples
+  switch (f.dtype) {
+    case MSDA_F32: return launch_gather_pipe<float, 4, false, 2, true, 8, true>(g, stream);
+    case MSDA_F16:
+      if (d.h2) return launch_gather_pipe<__half, 8, false, 2, true, 8, true, true>(g, stream);
+      return launch_gather_pipe<__half, 8, false, 2, true, 8, true>(g, stream);
+    default: return launch_gather_pipe<__nv_bfloat16, 8, false, 2, true, 8, true>(g, stream);
+  }
+}
 
 cudaError_t reset_exact_workspace(const ExactWorkspace& w, cudaStream_t stream) {
   return cudaMemsetAsync(w.status, 0, sizeof(DevStatus), stream);

@@ -32,4 +32,21 @@ inline cudaError_t launch_csr_fast(const msda_features_t& f, const msda_csr_plan
   return launch_gather_exact(f, p, MSDA_FAST, w, out, empty, stream, 0, 0, normalize ? 1 : 0);
 }
 
+// FAST on the dense Sparse4D layout through the pipelined gather (records
+// built from the sampling locations on the fly, no plan pass).
+// cudaErrorNotSupported when the shape does not fit (G > 8, a lane's channels
+// straddling groups, misalignment): the caller then uses its own kernel.
+struct DenseFastSpec {
+  const float* loc;  // [batch * Q, P, cams, 2]
+  const float* w;    // [batch * Q, P, cams, L, G]
+  int32_t Q, P, G, normalize;
+  float* wsum_out;      // [batch * Q, G] or null
+  float* wsum_scratch;  // [batch * Q, G] device scratch for split normalisation
+  bool h2;              // FAST_H2: half2 accumulation per camera (f16 storage; other dtypes ignore it)
+};
+// *normalize_pending: the cameras were split across warps and out holds
+// unnormalised sums; the caller divides by wsum (out or scratch) per group.
+cudaError_t launch_gather_dense_fast(const msda_features_t& f, const DenseFastSpec& d, DevStatus* status, float* out,
+                                     cudaStream_t stream, bool* normalize_pending);
+
 }  // namespace msda

@@ -58,7 +58,8 @@ def test_dense_exact_matches_reference_golden(golden, cuda_dev):
 
 
 @pytest.mark.parametrize("groups,channels,cams,levels,normalize", [
-    (8, 256, 6, 4, False), (8, 256, 3, 4, True), (1, 64, 2, 3, False), (4, 32, 4, 2, True), (2, 8, 2, 2, False)])
+    (8, 256, 6, 4, False), (8, 256, 3, 4, True), (1, 64, 2, 3, False), (4, 32, 4, 2, True), (2, 8, 2, 2, False),
+    (16, 256, 3, 4, True), (2, 128, 2, 4, True)])
 def test_dense_fast_fp32_tolerance(cuda_dev, groups, channels, cams, levels, normalize):
     import torch
 
