@@ -169,11 +169,11 @@ def project_case(reps, dev, cams=6, C=256, G=8, Q=900):
     K, R, T = ring(cams)
     camd = ops.Cameras(K, R, T, device=dev)
     anchors = anchors_for(Q, dev).unsqueeze(0)
-    offs = (torch.rand((6, 3), generator=torch.Generator().manual_seed(3)) * 2 - 1)
+    offs = (torch.rand((6, 3), generator=torch.Generator().manual_seed(3)) * 2 - 1).to(dev)
+    strides = torch.tensor([4.0, 8.0, 16.0, 32.0], device=dev)  # resident: no per-call host copies
     _, w = make_dense_inputs(1, Q, 13, cams, 4, G, dev)
     out = torch.empty((1, Q, C), device=dev)
-    fn = lambda: ops.msda_dense_project(feats, anchors, offs, camd, [4.0, 8.0, 16.0, 32.0], w, dt=0.1,  # noqa
-                                        out=out)
+    fn = lambda: ops.msda_dense_project(feats, anchors, offs, camd, strides, w, dt=0.1, out=out)  # noqa: E731
     med, best = time_fn(fn, reps, flush=True)
     return {"config": "cfg1-project", "path": "msda_dense_project (fused keypoints + projection)",
             "precision": "fast", "dtype": "float32", "cams": cams, "latency_us": med * 1e3, "best_us": best * 1e3,
