@@ -41,6 +41,11 @@ struct OaeArgs {
   float* out;            // [Q, C]
   uint8_t* occluded;     // [Q]
   DevStatus* status;
+  // camera groups (oae_warp_kernel<.., SPLIT>): CTA (q, grp) takes cameras
+  // [grp * kOaeWarps, (grp + 1) * kOaeWarps) and writes its partial sums
+  int32_t n_grp;
+  double* part;     // [Q, n_grp, C] sum_c v_c view_c over the group's valid views
+  double* part_vt;  // [Q, n_grp] sum_c v_c over the same views
 };
 
 // block-wide sum of one double per thread (blockDim multiple of 32, <= 1024)
@@ -186,7 +191,11 @@ constexpr int kOaeWarps = 8;
 constexpr int kOaeLevels = 4;   // levels loaded together (more are looped)
 constexpr int kOaeMaxRecs = 64;  // keypoints x levels staged per camera
 
-template <typename T, int VEC>
+// SPLIT: with many cameras one CTA per query leaves a ragged last wave (900
+// CTAs at 2 per SM = 3.04 waves on 148 SMs); CTAs of (query, group of
+// kOaeWarps cameras) — one camera per warp — write per-group partials (f64,
+// fixed order) that oae_finish_kernel reduces in group order: deterministic.
+template <typename T, int VEC, bool SPLIT = false>
 __global__ void __launch_bounds__(kOaeWarps * 32, 2) oae_warp_kernel(OaeArgs a) {
   constexpr int NV = VEC * (int)sizeof(T) / 16;
   constexpr int LV = NV >= 2 ? 2 : kOaeLevels;  // levels in flight: bounded by registers
@@ -196,7 +205,9 @@ __global__ void __launch_bounds__(kOaeWarps * 32, 2) oae_warp_kernel(OaeArgs a) 
   __shared__ double s_vt[kOaeWarps];
   __shared__ double s_red[kOaeWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q = blockIdx.x;
+  const int q = SPLIT ? (int)(blockIdx.x / a.n_grp) : (int)blockIdx.x;
+  const int grp = SPLIT ? (int)(blockIdx.x - (int64_t)q * a.n_grp) : 0;
+  const int cam_end = SPLIT ? min(a.cams, (grp + 1) * kOaeWarps) : a.cams;
   const int c0 = lane * VEC;
   const size_t row_bytes = (size_t)a.C * sizeof(T);
   const char* feat = reinterpret_cast<const char*>(a.feat) + (size_t)c0 * sizeof(T);
@@ -217,7 +228,7 @@ __global__ void __launch_bounds__(kOaeWarps * 32, 2) oae_warp_kernel(OaeArgs a) 
   const float inv_l = 1.0f / (float)a.L;  // level mean folded into the bilinear weights
   double vt = 0.0;
 
-  for (int cam = warp; cam < a.cams; cam += kOaeWarps) {
+  for (int cam = grp * kOaeWarps + warp; cam < cam_end; cam += kOaeWarps) {
     double up = 0.0, vp = 0.0;
     const bool ok = lane < a.P &&
                     project_f64(a.K + cam * 4, a.R + cam * 9, a.T + cam * 3, s_kp + 3 * min(lane, a.P - 1), up, vp);
@@ -337,6 +348,17 @@ __global__ void __launch_bounds__(kOaeWarps * 32, 2) oae_warp_kernel(OaeArgs a) 
   double total = 0.0;
 #pragma unroll
   for (int w = 0; w < kOaeWarps; ++w) total += s_vt[w];
+  if constexpr (SPLIT) {  // the group's partials; oae_finish_kernel completes the query
+    double* pp = a.part + ((int64_t)q * a.n_grp + grp) * a.C;
+    for (int c = threadIdx.x; c < a.C; c += blockDim.x) {
+      double f = 0.0;
+#pragma unroll
+      for (int w = 0; w < kOaeWarps; ++w) f += (double)s_fused[w][c];
+      pp[c] = f;
+    }
+    if (threadIdx.x == 0) a.part_vt[(int64_t)q * a.n_grp + grp] = total;
+    return;
+  }
   float* o = a.out + (int64_t)q * a.C;
   if (!(total > 1e-3)) {  // AllOccluded -> keep the memory embedding (oae.py:159-164)
     for (int c = threadIdx.x; c < a.C; c += blockDim.x) o[c] = a.memory[(int64_t)q * a.C + c];
@@ -366,9 +388,59 @@ __global__ void __launch_bounds__(kOaeWarps * 32, 2) oae_warp_kernel(OaeArgs a) 
   if (threadIdx.x == 0) a.occluded[q] = 0;
 }
 
+// one CTA per query: sum the groups' partials in group order, then the
+// fused / total, AllOccluded and L2-normalisation steps of oae_warp_kernel
+__global__ void __launch_bounds__(256) oae_finish_kernel(OaeArgs a) {
+  __shared__ double s_red[8];
+  const int q = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* pv = a.part_vt + (int64_t)q * a.n_grp;
+  double total = 0.0;
+  for (int g = 0; g < a.n_grp; ++g) total += pv[g];
+  float* o = a.out + (int64_t)q * a.C;
+  if (!(total > 1e-3)) {  // AllOccluded -> keep the memory embedding (oae.py:159-164)
+    for (int c = threadIdx.x; c < a.C; c += blockDim.x) o[c] = a.memory[(int64_t)q * a.C + c];
+    if (threadIdx.x == 0) a.occluded[q] = 1;
+    return;
+  }
+  const double* pp = a.part + (int64_t)q * a.n_grp * a.C;
+  double sq = 0.0;
+  double f[4];  // C <= 4 * 256 (kOaeMaxC)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = threadIdx.x + i * 256;
+    f[i] = 0.0;
+    if (c < a.C) {
+      for (int g = 0; g < a.n_grp; ++g) f[i] += pp[(int64_t)g * a.C + c];
+      f[i] /= total;
+      sq += f[i] * f[i];
+    }
+  }
+#pragma unroll
+  for (int o2 = 16; o2 > 0; o2 >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o2);
+  if (lane == 0) s_red[warp] = sq;
+  __syncthreads();
+  double norm2 = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) norm2 += s_red[w];
+  const double norm = sqrt(norm2);
+  if (!(norm >= 1e-12)) set_status(a.status, MSDA_BAD_ARG, q);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = threadIdx.x + i * 256;
+    if (c < a.C) o[c] = (float)(f[i] / norm);
+  }
+  if (threadIdx.x == 0) a.occluded[q] = 0;
+}
+
 template <typename T, int VEC>
 cudaError_t launch_oae_warp(const OaeArgs& a, cudaStream_t s) {
   if (a.Q == 0) return cudaSuccess;
+  if (a.n_grp > 1) {
+    oae_warp_kernel<T, VEC, true><<<(unsigned)((int64_t)a.Q * a.n_grp), kOaeWarps * 32, 0, s>>>(a);
+    if (cudaGetLastError() != cudaSuccess) return cudaErrorLaunchFailure;
+    oae_finish_kernel<<<a.Q, 256, 0, s>>>(a);
+    return cudaGetLastError();
+  }
   oae_warp_kernel<T, VEC><<<a.Q, kOaeWarps * 32, 0, s>>>(a);
   return cudaGetLastError();
 }
@@ -395,11 +467,13 @@ using namespace msda;
 
 extern "C" {
 
+// status | per-(query, camera group) partials (split path, cams > kOaeWarps)
+static size_t oae_groups(int32_t n_cams) { return n_cams > kOaeWarps ? (n_cams + kOaeWarps - 1) / kOaeWarps : 1; }
+
 size_t msda_oae_workspace_size(int32_t n_queries, int32_t n_cams, int32_t channels) {
-  (void)n_queries;
-  (void)n_cams;
-  (void)channels;
-  return kStatusBytes;
+  const size_t g = oae_groups(n_cams);
+  if (g <= 1 || n_queries <= 0 || channels <= 0) return kStatusBytes;
+  return kStatusBytes + align_up((size_t)n_queries * g * channels * 8, 256) + align_up((size_t)n_queries * g * 8, 256);
 }
 
 int32_t msda_oae_pool(const msda_features_t* f, int32_t n_queries, const float* anchors, int32_t n_learned,
@@ -438,6 +512,13 @@ int32_t msda_oae_pool(const msda_features_t* f, int32_t n_queries, const float* 
   a.occluded = all_occluded;
   a.status = reinterpret_cast<DevStatus*>(workspace);
   if (cudaMemsetAsync(workspace, 0, sizeof(DevStatus), s) != cudaSuccess) return MSDA_CUDA_ERROR;
+  a.n_grp = 1;
+  if (oae_groups(f->n_cams) > 1 && workspace_bytes >= msda_oae_workspace_size(n_queries, f->n_cams, f->channels)) {
+    a.n_grp = (int32_t)oae_groups(f->n_cams);
+    char* p = reinterpret_cast<char*>(workspace) + kStatusBytes;
+    a.part = reinterpret_cast<double*>(p);
+    a.part_vt = reinterpret_cast<double*>(p + align_up((size_t)n_queries * a.n_grp * f->channels * 8, 256));
+  }
   const uintptr_t al = reinterpret_cast<uintptr_t>(f->data);
   cudaError_t e;
   const int C = f->channels;

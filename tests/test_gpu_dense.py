@@ -223,16 +223,17 @@ def test_oae_channel_mismatch(cuda_dev):
                      torch.zeros(1, 4))
 
 
-@pytest.mark.parametrize("dt", ["float32", "bfloat16"])
-def test_oae_pool_production_kernel(cuda_dev, dt):
-    """C = 256 takes the warp-per-camera online-softmax kernel; compare with
+@pytest.mark.parametrize("dt,cams", [("float32", 10), ("bfloat16", 10), ("float32", 6), ("bfloat16", 17)])
+def test_oae_pool_production_kernel(cuda_dev, dt, cams):
+    """C = 256 takes the warp-per-camera online-softmax kernel (more than 8
+    cameras: per-camera-group CTAs + the finishing reduction); compare with
     the oracle (oae.py:81-164 restated) on the features the GPU sees."""
     import torch
 
     from paper_2601_10819_b200 import ops
 
     rng = np.random.default_rng(61)
-    cams, n_levels, channels = 10, 4, 256
+    n_levels, channels = 4, 256
     strides = [4.0, 8.0, 16.0, 32.0]
     grids, shape = {}, np.zeros((cams, n_levels, 2), dtype=np.int32)
     for c in range(cams):
