@@ -18,7 +18,11 @@ if [ "${NCU:-1}" = "1" ]; then
       python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 1 > $OUT/ncu_full.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:plan_canon -s 3 -c 1 -o $OUT/prof_plan \
       python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 1 > $OUT/ncu_full_plan.log 2>&1
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:dense_ -s 3 -c 1 -o $OUT/prof_dense \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:gather_pipe -s 3 -c 1 -o $OUT/prof_dense \
       python tools/bench_paths.py --only cfg3 --reps 2 > $OUT/ncu_full_dense.log 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:gather_pipe -s 3 -c 1 -o $OUT/prof_dense_cfg2 \
+      python tools/bench_paths.py --only cfg2d --reps 2 > $OUT/ncu_full_dense_cfg2.log 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:oae_warp -s 3 -c 1 -o $OUT/prof_oae \
+      python tools/bench_paths.py --only cfg4 --reps 2 > $OUT/ncu_full_oae.log 2>&1
 fi
 echo done > $OUT/done
