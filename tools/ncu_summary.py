@@ -103,7 +103,13 @@ def summarise_launches(csv_path: Path, dst: Path):
     # exact gather (RAW = 0); everything else in the process (the fast-precision
     # leg, the e2e host-path fetch, torch helpers) is listed separately
     def in_step(k):
-        return "plan_canon_kernel" in k or ("gather_pipe_kernel" in k and ", 0, 1>" in k)
+        if "plan_canon_kernel" in k:
+            return True
+        if "gather_pipe_kernel<" not in k:
+            return False
+        # template arguments <T, VEC, HALF, D, RAW, GW, DENSE, HACC>: the exact CSR gather has RAW = 0, GW = 1
+        args = [a.strip() for a in k.split("gather_pipe_kernel<", 1)[1].split(">", 1)[0].split(",")]
+        return len(args) >= 6 and args[4] == "0" and args[5] == "1" and (len(args) < 7 or args[6] == "0")
 
     def table(keys):
         total = sum(tot[k] for k in keys) or 1.0

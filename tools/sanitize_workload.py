@@ -1,5 +1,6 @@
 # compute-sanitizer workload: one small call of every production kernel (exact / fast / exact_half CSR,
-# dense fast / fast_h2 / exact, fused projection, OAE, visibility, painting, association) in f32 / f16 / bf16.
+# dense fast / fast_h2 / exact incl. the camera-group split, fused projection, OAE (one CTA per query and per camera
+# group), visibility, painting, association) in f32 / f16 / bf16.
 # Run: compute-sanitizer --tool {memcheck,racecheck,synccheck,initcheck} python tools/sanitize_workload.py
 # Small invocations of every production kernel, for compute-sanitizer runs.
 import sys
@@ -40,6 +41,29 @@ for dt in (torch.float32, torch.float16, torch.bfloat16):
     vis = torch.rand((16, 2), device=dev)
     mem = torch.nn.functional.normalize(torch.randn((16, 256), device=dev), dim=1)
     ops.oae_pool(feats, anchors[0], offs, cams, [4.0, 8.0, 16.0, 32.0], desc, vis, mem)
+# more than one camera group: the dense pipelined gather's split path (red.add partials + group normalise,
+# also with the caller's weight sums) and the OAE (query, camera group) CTAs + finishing kernel
+wl9 = BenchWorkload(cameras=9, levels=4, channels=256, queries=8, points_per_query=13, level0_size=(32, 88))
+gw9 = generate_workload(wl9)
+rng = np.random.default_rng(2)
+K9 = np.array([[300.0, 300.0, 352.0, 128.0]] * 9)
+R9 = np.stack([np.eye(3)] * 9).reshape(9, 9)
+T9 = np.array([[0.0, 0.0, 10.0 + c] for c in range(9)])
+cams9 = ops.Cameras(K9, R9, T9, device=dev)
+for dt in (torch.float32, torch.float16, torch.bfloat16):
+    f9 = ops.DeviceFeatures(t(gw9.table).to(dt), t(gw9.spatial_shape), t(gw9.tile_start.reshape(9, 4)))
+    loc9 = t(rng.uniform(0, 1, (1, 8, 13, 9, 2)).astype(np.float32))
+    w9 = t(rng.uniform(0.01, 1, (1, 8, 13, 9, 4, 8)).astype(np.float32))
+    for prec in ("fast", "fast_h2"):
+        if prec == "fast_h2" and dt is not torch.float16:
+            continue
+        ops.deformable_aggregation(f9, None, None, loc9, w9, precision=prec, normalize=True, check=True)
+    ops.deformable_aggregation_partial(f9, loc9, w9, precision="fast")
+    a9 = torch.zeros((8, 10), device=dev)
+    a9[:, 3:6] = torch.tensor([0.6, 0.6, 1.8])
+    ops.oae_pool(f9, a9, np.zeros((6, 3), np.float32), cams9, [4.0, 8.0, 16.0, 32.0], torch.randn((8, 256), device=dev),
+                 torch.rand((8, 9), device=dev),
+                 torch.nn.functional.normalize(torch.randn((8, 256), device=dev), dim=1))
 ops.visibility(cams, [[704, 256]] * 2, [[0, 0, 0, 1, 1, 1, 0], [0.5, 0, 1, 1, 1, 1, 0.3]], grid=16)
 sc = ops.PaintScene(cams, [[704, 256]] * 2, [8.0, 16.0], 32, [[0, 0, 0, 1, 1, 1, 0], [0.5, 0, 1, 1, 1, 1, 0.3]], 1,
                     np.ones((1, 32)) / np.sqrt(32))
