@@ -832,11 +832,50 @@ cudaError_t launch_gather_pipe(const GatherArgs& g, cudaStream_t stream) {
   return cudaLaunchKernelEx(&cfg, gather_pipe_kernel<T, VEC, HALF, D, RAW, GW, DENSE, HACC>, g);
 }
 
+// resident one-warp CTAs of gather_pipe_kernel<..., D, ..., GW> on the device
+template <typename T, int VEC, bool HALF, int D, int GW>
+int64_t pipe_slots() {
+  static std::atomic<int64_t> cached[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64) {
+    const int64_t c = cached[dev].load(std::memory_order_relaxed);
+    if (c > 0) return c;
+  }
+  constexpr int BYTES = VEC * (int)sizeof(T);
+  const int smem = kPipeWarps * PipeSmem<BYTES, D, GW>::kPerWarp;
+  int per_sm = 0, sms = 148;
+  cudaFuncSetAttribute(gather_pipe_kernel<T, VEC, HALF, D, false, GW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gather_pipe_kernel<T, VEC, HALF, D, false, GW>,
+                                                    kPipeWarps * 32, smem) != cudaSuccess)
+    per_sm = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t slots = (int64_t)per_sm * sms * kPipeWarps;
+  if (dev >= 0 && dev < 64 && slots > 0) cached[dev].store(slots, std::memory_order_relaxed);
+  return slots;
+}
+
+// EXACT (16-B lanes): a query's canonical accumulation is one sequential
+// chain per warp, so a grid that spills a few warps into a second wave costs
+// a whole extra chain (cfg1 dense EXACT: 1800 warps vs 12 x 148 resident at
+// ring depth 7 -> 160.6 us; depth 6, 13 per SM -> 126 us).  Use the deepest
+// ring whose residency still holds every warp at once.
+template <typename T, int VEC, bool HALF, int GW>
+cudaError_t launch_exact_pipe(const GatherArgs& g, cudaStream_t stream) {
+  const int64_t warps = g.n_queries * (g.C / VEC / 32);
+  if (warps > pipe_slots<T, VEC, HALF, 7, GW>()) {
+    if (warps <= pipe_slots<T, VEC, HALF, 6, GW>()) return launch_gather_pipe<T, VEC, HALF, 6, false, GW>(g, stream);
+    if (warps <= pipe_slots<T, VEC, HALF, 5, GW>()) return launch_gather_pipe<T, VEC, HALF, 5, false, GW>(g, stream);
+  }
+  return launch_gather_pipe<T, VEC, HALF, 7, false, GW>(g, stream);
+}
+
 template <typename T, int VEC, bool HALF>
 cudaError_t launch_gather(const GatherArgs& g, cudaStream_t stream, bool raw) {
   if (g.n_groups > 1) {  // per-group weights (dense EXACT, one pass): pipelined kernel only
     if ((g.C / VEC) % 32 != 0 || g.C % VEC != 0 || g.n_groups > 8) return cudaErrorNotSupported;
-    if constexpr (VEC * sizeof(T) == 16) return launch_gather_pipe<T, VEC, HALF, 7, false, 8>(g, stream);
+    if constexpr (VEC * sizeof(T) == 16) return launch_exact_pipe<T, VEC, HALF, 8>(g, stream);
     else return launch_gather_pipe<T, VEC, HALF, 12, false, 8>(g, stream);
   }
   if ((g.C / VEC) % 32 == 0 && g.C % VEC == 0) {
@@ -846,7 +885,7 @@ cudaError_t launch_gather(const GatherArgs& g, cudaStream_t stream, bool raw) {
         else return launch_gather_pipe<T, VEC, HALF, 12, true>(g, stream);
       }
     }
-    if constexpr (VEC * sizeof(T) == 16) return launch_gather_pipe<T, VEC, HALF, 7, false>(g, stream);
+    if constexpr (VEC * sizeof(T) == 16) return launch_exact_pipe<T, VEC, HALF, 1>(g, stream);
     else return launch_gather_pipe<T, VEC, HALF, 12, false>(g, stream);
   }
   if (raw) return cudaErrorNotSupported;
