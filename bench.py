@@ -260,6 +260,16 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def rank_device(local_rank):
+    """cuda:local_rank; BENCH_SHARE_GPU=1 (multi-rank smoke test on a one-GPU box) folds every rank onto the
+    visible GPUs and uses gloo, since NCCL refuses two ranks on one device.  Never set for a measurement."""
+    import torch
+
+    if os.environ.get("BENCH_SHARE_GPU") == "1":
+        return torch.device("cuda", local_rank % torch.cuda.device_count()), "gloo"
+    return torch.device("cuda", local_rank), "nccl"
+
+
 def run_ours(args, cfg, rank, local_rank, world):
     import torch
     import torch.distributed as dist
@@ -267,10 +277,10 @@ def run_ours(args, cfg, rank, local_rank, world):
     from paper_2601_10819_b200 import features as F
     from paper_2601_10819_b200 import ops
 
-    dev = torch.device("cuda", local_rank)
+    dev, backend = rank_device(local_rank)
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(backend, device_id=dev)
 
     def barrier():
         if world > 1:
@@ -301,7 +311,7 @@ def run_ours(args, cfg, rank, local_rank, world):
     torch.cuda.synchronize(dev)
 
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-    smi_index = vis.split(",")[local_rank] if vis else str(local_rank)
+    smi_index = vis.split(",")[dev.index] if vis else str(dev.index)
     clocks = ClockSampler(smi_index)
     clocks.start()
     time.sleep(0.2)
@@ -376,7 +386,7 @@ def run_ours(args, cfg, rank, local_rank, world):
     for i in range(args.warmup + e2e_k):
         barrier()
         t1 = time.perf_counter()
-        out_h, _ = F.msda_optimized(pyrs, plan_h, device=local_rank)
+        out_h, _ = F.msda_optimized(pyrs, plan_h, device=dev.index)
         dt = time.perf_counter() - t1
         if i >= args.warmup:
             e2e_times.append(dt)
@@ -385,7 +395,7 @@ def run_ours(args, cfg, rank, local_rank, world):
         tt = torch.tensor([e2e_s], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
-    h2d = F.last_h2d_bytes(local_rank)  # whole grids copied + corner rows fetched from the sparse ones
+    h2d = F.last_h2d_bytes(dev.index)  # whole grids copied + corner rows fetched from the sparse ones
     pcie = pcie_h2d_ceiling(dev)
     d2h = wl.queries * wl.channels * 4 + wl.queries
     same = out_h.tobytes() == out.cpu().numpy().tobytes()
@@ -485,10 +495,10 @@ def run_dense_scaling(args, cfg, rank, local_rank, world):
     from paper_2601_10819_b200 import ops
     from paper_2601_10819_b200.dist import CameraShardedAggregation, camera_range, shard_streams
 
-    dev = torch.device("cuda", local_rank)
+    dev, backend = rank_device(local_rank)
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(backend, device_id=dev)
     Q, P, G, C, L = 900, 13, 8, 256, 4
     gen = torch.Generator(device=dev).manual_seed(rank)
 
