@@ -406,3 +406,28 @@ def test_dense_exact_full_size_cfg1(c_oracle, cuda_dev, dt):
         plan = _dense_csr_vectorized(shape, loc, wts, g)
         ref, _ = c_oracle.msda_c(np.ascontiguousarray(seen[:, g * cpg:(g + 1) * cpg]), tiles, 4, *plan)
         assert out[:, g * cpg:(g + 1) * cpg].tobytes() == ref.tobytes(), g
+
+
+@pytest.mark.parametrize("cams,precision", [(2, "fast"), (6, "fast"), (6, "exact"), (6, "fast_h2")])
+def test_dense_zero_weight_sum_raises(cuda_dev, cams, precision):
+    """normalize=True with one (anchor, group) whose weights are all zero:
+    every path (one camera group, split camera groups + normalising pass,
+    exact) reports the zero sum; without normalisation the call succeeds and
+    that group's channels are exactly zero."""
+    import torch
+
+    from paper_2601_10819_b200 import ops
+
+    rng = np.random.default_rng(17)
+    grids, shape, loc, wts = helpers.make_dense(rng, bs=1, n_q=3, n_p=13, cams=cams, n_levels=4, groups=8,
+                                                channels=256, size_lo=6, size_hi=20)
+    wts[0, 1, ..., 5] = 0.0
+    dt = torch.float16 if precision == "fast_h2" else torch.float32
+    feats, table, tiles = _feats(ops, torch, grids, shape, cuda_dev, dtype=dt)
+    t = lambda a: torch.from_numpy(a).to(cuda_dev)  # noqa: E731
+    with pytest.raises(ValueError, match="sum to zero"):
+        ops.deformable_aggregation(feats, None, None, t(loc), t(wts), precision=precision, normalize=True, check=True)
+    out = ops.deformable_aggregation(feats, None, None, t(loc), t(wts), precision=precision, normalize=False,
+                                     check=True).cpu().numpy()
+    assert not out[0, 1, 5 * 32:6 * 32].any()
+    assert np.isfinite(out).all()
