@@ -431,3 +431,39 @@ def test_dense_zero_weight_sum_raises(cuda_dev, cams, precision):
                                      check=True).cpu().numpy()
     assert not out[0, 1, 5 * 32:6 * 32].any()
     assert np.isfinite(out).all()
+
+
+@pytest.mark.parametrize("cams,levels,dt", [
+    (6, [(64, 176), (32, 88), (16, 44), (8, 22)], "float32"),      # cfg1: 2 camera groups
+    (16, [(270, 480), (135, 240), (68, 120), (34, 60)], "float32"),  # cfg2 shape: 4 camera groups, maps >> L2
+    (32, [(64, 176), (32, 88), (16, 44), (8, 22)], "bfloat16"),    # cfg4 MSDA part
+    (64, [(64, 176), (32, 88), (16, 44), (8, 22)], "float16")])    # cfg3 per layer
+def test_dense_fast_full_size_vs_exact(cuda_dev, cams, levels, dt):
+    """BASELINE shapes at full size (900 anchors, 13 points, C = 256, G = 8):
+    the pipelined FAST gather (camera groups, red.add partials, normalising
+    pass) against the bit-exact path on the same device features — exact is
+    pinned to the C oracle at cfg1 above.  fp32: 1e-4 relative; f16/bf16
+    storage with f32 products: 1e-4 too (same rounded inputs); FAST_H2 (half2
+    products and partials): the north_star's 1e-2."""
+    import torch
+
+    from paper_2601_10819_b200 import ops
+
+    rng = np.random.default_rng(97 + cams)
+    C, G, Q, P = 256, 8, 900, 13
+    dtype = getattr(torch, dt)
+    n_rows = cams * sum(h * w for h, w in levels)
+    table = (torch.rand((1, n_rows, C), generator=torch.Generator().manual_seed(cams)) * 2 - 1).to(cuda_dev, dtype)
+    shape = np.array([levels] * cams, dtype=np.int32)
+    start = np.cumsum([0] + [h * w for _ in range(cams) for h, w in levels])[:-1].reshape(cams, 4)
+    feats = ops.DeviceFeatures(table, torch.from_numpy(shape), torch.from_numpy(start.astype(np.int64)))
+    loc = torch.from_numpy(rng.uniform(-0.02, 1.02, (1, Q, P, cams, 2)).astype(np.float32)).to(cuda_dev)
+    logits = torch.from_numpy(rng.standard_normal((1, Q, P * cams * 4, G)).astype(np.float32)).to(cuda_dev)
+    wts = torch.softmax(logits, dim=2).reshape(1, Q, P, cams, 4, G).contiguous()
+    exact = ops.deformable_aggregation(feats, None, None, loc, wts, precision="exact", normalize=True, check=True)
+    fast = ops.deformable_aggregation(feats, None, None, loc, wts, precision="fast", normalize=True, check=True)
+    scale = exact.abs().max().item()
+    assert (fast - exact).abs().max().item() <= 1e-4 * scale
+    if dt == "float16":
+        h2 = ops.deformable_aggregation(feats, None, None, loc, wts, precision="fast_h2", normalize=True, check=True)
+        assert (h2 - exact).abs().max().item() <= 1e-2 * max(1.0, scale)
