@@ -480,6 +480,9 @@ DENSE_CONFIGS = {
     # cfg5 (BASELINE configs[4]): 512 cameras of the cfg1 per-camera shape, fp16, Sparse4D dense FAST path
     "cfg5-stream": dict(cams=512, scene=32, shard="stream",
                         desc="512 cams as 16 scenes x 32 cams, fp16, dense FAST, scenes dealt round-robin to ranks"),
+    "cfg5-camera-peer": dict(cams=512, scene=512, shard="camera", transport="peer",
+                             desc="one 512-cam scene, fp16, dense FAST, cameras split across ranks, partials pushed "
+                                  "into every rank's buffer over NVLink (CUDA IPC, peer.cu) instead of NCCL"),
     "cfg5-camera": dict(cams=512, scene=512, shard="camera",
                         desc="one 512-cam scene, fp16, dense FAST, cameras split across ranks + NCCL partial-sum "
                              "all-reduce of [Q, C]"),
@@ -526,10 +529,11 @@ def run_dense_scaling(args, cfg, rank, local_rank, world):
         lo, hi = camera_range(cfg["cams"], rank, world)
         feats = scene_feats(hi - lo)
         loc, w = inputs(hi - lo)  # this rank's cameras of the scene's sampling plan
-        agg = CameraShardedAggregation.for_device_features(cfg["cams"], feats, precision="fast")
+        agg = CameraShardedAggregation.for_device_features(cfg["cams"], feats, precision="fast",
+                                                           transport=cfg.get("transport", "collective"))
 
         def step():
-            agg(loc, w, local_inputs=True)
+            agg(loc, w, local_inputs=True, check=False)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
@@ -554,6 +558,8 @@ def run_dense_scaling(args, cfg, rank, local_rank, world):
             "config": {"workload": args.config, "desc": cfg["desc"], "queries": Q, "points": P, "groups": G,
                        "channels": C, "levels": CFG1_LEVELS},
             "streams_at_30fps_6layers": int(cfg["cams"] / (30 * 6 * ms / 1e3))}), flush=True)
+    if cfg["shard"] == "camera":
+        agg.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -138,6 +138,30 @@ int32_t msda_dense_partial(const msda_features_t *feat, int32_t n_queries, int32
 int32_t msda_dense_normalize(float *out, const float *weight_sums, int64_t n_queries, int32_t channels,
                              int32_t n_groups, void *workspace /* >= 256 B */, void *stream);
 
+/* Camera-sharded all-reduce over peer memory (NVLink), the alternative to
+ * msda_dense_partial -> NCCL all-reduce -> msda_dense_normalize: every rank
+ * pushes its partial numerators [rows, C] and weight sums [rows, G] into
+ * every rank's symmetric buffer (float4 red.add through CUDA-IPC mappings),
+ * signals with a system-scope release counter, waits for all ranks and
+ * writes out = num / wsum per group (normalize) or num.  Buffers:
+ * msda_peer_alloc(msda_peer_buffer_size(rows, C, G)) on every rank, handles
+ * exchanged with msda_ipc_handle / msda_ipc_open (64 bytes each);
+ * peer_buffers[r] = rank r's buffer as mapped here (own buffer at [rank]).
+ * epoch: 1, 2, 3, ... identical on every rank, one per call.  A rank that
+ * never arrives makes the call report MSDA_CUDA_ERROR (status word) after a
+ * bounded wait. */
+#define MSDA_IPC_HANDLE_BYTES 64
+size_t msda_peer_buffer_size(int64_t rows, int32_t channels, int32_t groups);
+int32_t msda_peer_alloc(size_t bytes, void **ptr);
+int32_t msda_peer_free(void *ptr);
+int32_t msda_ipc_handle(const void *ptr, void *handle /* MSDA_IPC_HANDLE_BYTES */);
+int32_t msda_ipc_open(const void *handle, void **ptr);
+int32_t msda_ipc_close(void *ptr);
+int32_t msda_peer_allreduce_normalize(const float *num, const float *weight_sums, void *const *peer_buffers,
+                                      int32_t world, int32_t rank, uint32_t epoch, int64_t rows, int32_t channels,
+                                      int32_t groups, int32_t normalize, float *out, float *wsum_out,
+                                      void *workspace /* >= 256 B */, void *stream);
+
 /* Fused projection: anchors [bs, Q, 10] (x, y, z, w, l, h, yaw, vx, vy, vz),
  * learned_offsets [n_learned, 3] in [-1, 1], P = 7 + n_learned keypoints
  * (geometry.py:207-247), motion compensation by velocity*dt

@@ -79,3 +79,16 @@ def test_camera_range_partition():
             sizes = [b - a for a, b in ranges]
             assert max(sizes) - min(sizes) <= 1
     assert shard_streams(16, 1, 8) == [1, 9]
+
+
+def test_camera_sharded_transport_validation():
+    """Only the all-reduce ("collective") and peer-memory ("peer") transports exist."""
+    import pytest
+
+    from paper_2601_10819_b200.dist import CameraShardedAggregation
+
+    with pytest.raises(ValueError, match="unknown transport"):
+        CameraShardedAggregation(4, lambda loc, w: None, transport="nvshmem")
+    agg = CameraShardedAggregation(4, lambda loc, w: None)
+    assert agg.transport == "collective" and agg.world == 1 and (agg.cam_lo, agg.cam_hi) == (0, 4)
+    agg.close()  # no peer buffers: a no-op
