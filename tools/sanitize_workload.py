@@ -1,6 +1,6 @@
 # compute-sanitizer workload: one small call of every production kernel (exact / fast / exact_half CSR,
 # dense fast / fast_h2 / exact incl. the camera-group split, fused projection, OAE (one CTA per query and per camera
-# group), visibility, painting, association) in f32 / f16 / bf16.
+# group), visibility, painting, association, the peer-memory exchange) in f32 / f16 / bf16.
 # Run: compute-sanitizer --tool {memcheck,racecheck,synccheck,initcheck} python tools/sanitize_workload.py
 # Small invocations of every production kernel, for compute-sanitizer runs.
 import sys
@@ -64,6 +64,13 @@ for dt in (torch.float32, torch.float16, torch.bfloat16):
     ops.oae_pool(f9, a9, np.zeros((6, 3), np.float32), cams9, [4.0, 8.0, 16.0, 32.0], torch.randn((8, 256), device=dev),
                  torch.rand((8, 9), device=dev),
                  torch.nn.functional.normalize(torch.randn((8, 256), device=dev), dim=1))
+# peer-memory exchange (world 1: own buffer only), two epochs so both halves are used
+from paper_2601_10819_b200.dist import PeerExchange
+px = PeerExchange(16, 256, 8, dev)
+for _ in range(2):
+    px.allreduce_normalize(torch.rand((16, 256), device=dev), torch.rand((16, 8), device=dev) + 0.5, True)
+px.allreduce_normalize(torch.rand((16, 256), device=dev), torch.rand((16, 8), device=dev) + 0.5, False)
+px.close()
 ops.visibility(cams, [[704, 256]] * 2, [[0, 0, 0, 1, 1, 1, 0], [0.5, 0, 1, 1, 1, 1, 0.3]], grid=16)
 sc = ops.PaintScene(cams, [[704, 256]] * 2, [8.0, 16.0], 32, [[0, 0, 0, 1, 1, 1, 0], [0.5, 0, 1, 1, 1, 1, 0.3]], 1,
                     np.ones((1, 32)) / np.sqrt(32))
