@@ -79,6 +79,11 @@ __device__ double pairwise_block(const double* a, const double* b, int n) {
 // the recursive halving above 128 terms, unrolled as an explicit stack
 __device__ double pairwise_sum_sq(const double* a, const double* b, int n) {
   if (n <= 128) return pairwise_block(a, b, n);
+  if (n <= 256) {  // one halving, both halves <= 128: no stack (stays in registers)
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return __dadd_rn(pairwise_block(a, b, n2), pairwise_block(a + n2, b + n2, n - n2));
+  }
   // leaves in left-to-right order, combined bottom-up exactly like the recursion
   struct Node {
     int off, n, state;
