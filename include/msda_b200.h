@@ -150,6 +150,13 @@ int32_t msda_dense_normalize(float *out, const float *weight_sums, int64_t n_que
  * epoch: 1, 2, 3, ... identical on every rank, one per call.  A rank that
  * never arrives makes the call report MSDA_CUDA_ERROR (status word) after a
  * bounded wait. */
+/* Page-lock / release an existing host range (a memory-mapped FPYR payload:
+ * frames then go to the device as one DMA each, no staging copy).
+ * read_only != 0 for read-only mappings.  MSDA_CUDA_ERROR when the range
+ * cannot be registered (the caller stages through a pinned buffer). */
+int32_t msda_host_register(void *ptr, size_t bytes, int32_t read_only);
+int32_t msda_host_unregister(void *ptr);
+
 #define MSDA_IPC_HANDLE_BYTES 64
 size_t msda_peer_buffer_size(int64_t rows, int32_t channels, int32_t groups);
 int32_t msda_peer_alloc(size_t bytes, void **ptr);

@@ -76,6 +76,8 @@ SIGNATURES = {
     "msda_context_destroy": (None, [P]),
     "msda_context_last_h2d_bytes": (ctypes.c_longlong, [P]),
     "msda_csr_host": (I32, [P, P, P, I32, I32, I32, I32, I64, P, P, P, P, P, P, I32, I32, P, P]),
+    "msda_host_register": (I32, [P, SZ, I32]),
+    "msda_host_unregister": (I32, [P]),
     "msda_peer_buffer_size": (SZ, [I64, I32, I32]),
     "msda_peer_alloc": (I32, [SZ, ctypes.POINTER(P)]),
     "msda_peer_free": (I32, [P]),

@@ -211,6 +211,27 @@ struct msda_context {
 
 long long msda_context_last_h2d_bytes(const msda_context_t* ctx) { return ctx ? ctx->last_h2d_bytes : -1; }
 
+// Page-lock an existing host range (e.g. a memory-mapped FPYR file) so that
+// copies from it are single DMA transfers; read_only for PROT_READ mappings.
+int32_t msda_host_register(void* ptr, size_t bytes, int32_t read_only) {
+  if (!ptr || bytes == 0) return MSDA_BAD_ARG;
+  unsigned flags = cudaHostRegisterPortable | (read_only ? cudaHostRegisterReadOnly : 0u);
+  if (cudaHostRegister(ptr, bytes, flags) != cudaSuccess) {
+    cudaGetLastError();  // not sticky: the caller stages through a pinned buffer instead
+    return MSDA_CUDA_ERROR;
+  }
+  return MSDA_OK;
+}
+
+int32_t msda_host_unregister(void* ptr) {
+  if (!ptr) return MSDA_BAD_ARG;
+  if (cudaHostUnregister(ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return MSDA_CUDA_ERROR;
+  }
+  return MSDA_OK;
+}
+
 int32_t msda_context_create(int32_t device, msda_context_t** ctx) {
   if (!ctx) return MSDA_BAD_ARG;
   auto* c = new (std::nothrow) msda_context();

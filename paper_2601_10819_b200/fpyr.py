@@ -9,8 +9,10 @@ level-major, each grid ``H*W*C`` little-endian f32 in ``(H, W, C)`` order.
 A frame's payload is therefore *exactly* the channel-last concatenated
 feature table the kernels consume (rows camera-major then level-minor), so
 loading a frame onto the GPU is one contiguous host→device copy of a
-memory-mapped file region — no repacking.  ``FpyrReader.upload`` stages
-through a pinned buffer and copies asynchronously on the caller's stream.
+memory-mapped file region — no repacking.  ``FpyrReader.upload`` page-locks
+the mapping once and DMAs each frame straight from it, asynchronously on the
+caller's stream (or stages through a pinned buffer when the mapping cannot
+be registered).
 
 ``read_pyramid_sequence`` / ``write_pyramid_sequence`` mirror the reference
 functions (same format, same ValueErrors for bad magic, unknown version,
@@ -92,17 +94,56 @@ def read_header(buf) -> FpyrHeader:
 
 
 class FpyrReader:
-    """Memory-mapped FPYR file with zero-copy frame views and GPU upload."""
+    """Memory-mapped FPYR file with zero-copy frame views and GPU upload.
 
-    def __init__(self, path):
+    ``pin=True``: on the first upload the whole mapping is page-locked
+    (``msda_host_register``, read-only), so each frame goes to the device as
+    one DMA straight from the page cache; if the range cannot be registered
+    the upload stages through a pinned buffer (one host memcpy per frame)."""
+
+    def __init__(self, path, pin: bool = True):
         self.path = Path(path)
         self._fh = open(self.path, "rb")
         size = self.path.stat().st_size
-        self._mm = mmap.mmap(self._fh.fileno(), 0, access=mmap.ACCESS_READ) if size else b""
+        # a private (copy-on-write) mapping when pinning: the driver page-locks
+        # those, not read-only shared file mappings (measured on the B200 box)
+        access = mmap.ACCESS_COPY if pin else mmap.ACCESS_READ
+        self._mm = mmap.mmap(self._fh.fileno(), 0, access=access) if size else b""
         self.header = read_header(self._mm)
         self._staging = None
+        self._pin = pin
+        self._registered = None  # base address of the registered mapping
+        self._base = None  # numpy view of the whole mapping (keeps the address)
+
+    @property
+    def registered(self) -> bool:
+        return self._registered is not None
+
+    def _register(self):
+        import ctypes
+
+        from . import _lib as L
+
+        if not self._pin or self._registered is not None or not isinstance(self._mm, mmap.mmap):
+            return
+        self._pin = False  # one attempt
+        self._base = np.frombuffer(self._mm, dtype=np.uint8)
+        addr = self._base.ctypes.data
+        if L.lib().msda_host_register(ctypes.c_void_p(addr), self._base.nbytes, 0) == L.MSDA_OK:
+            self._registered = addr
 
     def close(self):
+        if self._registered is not None:
+            import ctypes
+
+            import torch
+
+            from . import _lib as L
+
+            torch.cuda.synchronize()  # no copy may still read the mapping
+            L.lib().msda_host_unregister(ctypes.c_void_p(self._registered))
+            self._registered = None
+        self._base = None
         if isinstance(self._mm, mmap.mmap):
             self._mm.close()
         self._fh.close()
@@ -122,8 +163,10 @@ class FpyrReader:
         if not 0 <= frame < h.n_frames:
             raise IndexError(f"frame {frame} out of range")
         off = h.payload_offset + frame * h.frame_bytes
-        return np.frombuffer(self._mm, dtype="<f4", count=h.rows * h.channels, offset=off).reshape(
+        view = np.frombuffer(self._mm, dtype="<f4", count=h.rows * h.channels, offset=off).reshape(
             h.rows, h.channels)
+        view.flags.writeable = False  # frames are immutable (features.py:67), whatever the mapping mode
+        return view
 
     def upload(self, frame: int, device="cuda", out=None, dtype=None, stream=None):
         """Copy one frame into a device table and wrap it as ``ops.DeviceFeatures``.
@@ -137,15 +180,26 @@ class FpyrReader:
 
         h = self.header
         src = self.frame_table(frame)
-        if self._staging is None or self._staging.shape != src.shape:
-            self._staging = torch.empty(src.shape, dtype=torch.float32, pin_memory=True)
         stream = stream or torch.cuda.current_stream(device)
-        stream.synchronize()  # the staging buffer may still feed a previous copy
-        self._staging.numpy()[...] = src
+        self._register()
         if out is None:
             out = torch.empty(src.shape, dtype=torch.float32, device=device)
+        if self._registered is not None:  # one DMA from the page-locked mapping
+            import warnings
+
+            with warnings.catch_warnings():  # read-only view: the copy only reads it
+                warnings.simplefilter("ignore", UserWarning)
+                host = torch.from_numpy(src)
+            with torch.cuda.stream(stream):
+                out.copy_(host, non_blocking=True)
+        else:
+            if self._staging is None or self._staging.shape != src.shape:
+                self._staging = torch.empty(src.shape, dtype=torch.float32, pin_memory=True)
+            stream.synchronize()  # the staging buffer may still feed a previous copy
+            self._staging.numpy()[...] = src
+            with torch.cuda.stream(stream):
+                out.copy_(self._staging, non_blocking=True)
         with torch.cuda.stream(stream):
-            out.copy_(self._staging, non_blocking=True)
             table = out if dtype in (None, torch.float32) else out.to(dtype)
         return DeviceFeatures(table, torch.from_numpy(h.spatial_shape()), torch.from_numpy(h.scale_start_index()))
 

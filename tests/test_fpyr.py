@@ -63,11 +63,17 @@ def test_reader_errors(golden, tmp_path):
 
 
 @pytest.mark.gpu
-def test_upload_frame_to_device(golden, tmp_path, cuda_dev):
+@pytest.mark.parametrize("pin", [True, False])
+def test_upload_frame_to_device(golden, tmp_path, cuda_dev, pin):
+    """pin=True: the mapping is page-locked and each frame is one DMA from it;
+    pin=False: staged through a pinned buffer.  Same bytes either way, every
+    frame, in any order."""
     path = tmp_path / "pyr.bin"
     path.write_bytes(golden("fpyr")["blob"].tobytes())
-    with fpyr.FpyrReader(path) as rd:
-        feats = rd.upload(2, device=cuda_dev)
-        host = rd.frame_table(2).copy()
-        np.testing.assert_array_equal(feats.table[0].cpu().numpy(), host)
+    with fpyr.FpyrReader(path, pin=pin) as rd:
+        for frame in (2, 0, 1, 2):
+            feats = rd.upload(frame, device=cuda_dev)
+            host = rd.frame_table(frame).copy()
+            np.testing.assert_array_equal(feats.table[0].cpu().numpy(), host)
         assert feats.spatial_shape.cpu().tolist() == [[[5, 6], [4, 5]], [[5, 6], [4, 5]]]
+        assert rd.registered == pin

@@ -14,8 +14,10 @@ import argparse
 import json
 import math
 import sys
+import time
 from pathlib import Path
 
+import numpy as np
 import torch
 
 ROOT = Path(__file__).resolve().parent.parent
@@ -273,6 +275,41 @@ def assoc_case(reps, dev, n_q=900, n_d=900, D=256):
             "pairs_per_s": n_q * n_d / (med / 1e3)}
 
 
+def fpyr_case(reps, dev, cams=6, C=256, frames=3):
+    """FPYR container (cfg1 shape, 92 MB per frame) -> device table, per frame:
+    one DMA from the page-locked mapping vs the pinned-staging path."""
+    import os
+    import tempfile
+
+    from paper_2601_10819_b200 import features as F
+    from paper_2601_10819_b200 import fpyr
+
+    rng = np.random.default_rng(5)
+    strides = [4.0, 8.0, 16.0, 32.0]
+    frame = {c: F.FeaturePyramid(c, [F.FeatureGrid(stride=s, values=rng.uniform(-1, 1, (h, w, C)).astype(np.float32))
+                                     for s, (h, w) in zip(strides, CFG1_LEVELS)]) for c in range(cams)}
+    path = os.path.join(tempfile.mkdtemp(), "cfg1.fpyr")
+    fpyr.write_pyramid_sequence(path, [frame] * frames)
+    res = {}
+    for pin in (True, False):
+        with fpyr.FpyrReader(path, pin=pin) as rd:
+            out = torch.empty((rd.header.rows, C), device=dev)
+            rd.upload(0, device=dev, out=out)
+            torch.cuda.synchronize()
+            ts = []
+            for i in range(reps):
+                t0 = time.perf_counter()
+                rd.upload(i % frames, device=dev, out=out)
+                torch.cuda.synchronize()
+                ts.append(time.perf_counter() - t0)
+            med = float(np.median(ts))
+            res["pinned_mapping" if pin else "staged"] = {"ms": med * 1e3, "gbs": out.numel() * 4 / med / 1e9,
+                                                          "registered": rd.registered}
+    os.remove(path)
+    return {"config": "fpyr-cfg1", "path": "FpyrReader.upload (frame -> channel-last device table)",
+            "frame_bytes": int(out.numel() * 4), **res}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
@@ -298,6 +335,7 @@ def main():
         "frame": lambda: frame_case(max(5, args.reps // 2), dev),
         "frame_fast": lambda: frame_case(max(5, args.reps // 2), dev, precision="fast"),
         "paint": lambda: paint_case(args.reps, dev),
+        "fpyr": lambda: fpyr_case(args.reps, dev),
         "assoc": lambda: assoc_case(args.reps, dev),
         "cfg4": lambda: oae_case(max(5, args.reps // 4), dev),
     }
