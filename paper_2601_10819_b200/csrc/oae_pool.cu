@@ -188,6 +188,7 @@ __global__ void oae_pool_kernel(OaeArgs a) {
 // summed across warps at the end (tolerance-level reassociation of Eq. 2).
 
 constexpr int kOaeWarps = 8;
+__device__ __align__(16) unsigned char g_oae_zero_row[kOaeMaxC * 4];  // zero-initialised at module load
 constexpr int kOaeLevels = 4;   // levels loaded together (more are looped)
 constexpr int kOaeMaxRecs = 64;  // keypoints x levels staged per camera
 
@@ -211,6 +212,8 @@ __global__ void __launch_bounds__(kOaeWarps * 32, 2) oae_warp_kernel(OaeArgs a) 
   const int c0 = lane * VEC;
   const size_t row_bytes = (size_t)a.C * sizeof(T);
   const char* feat = reinterpret_cast<const char*>(a.feat) + (size_t)c0 * sizeof(T);
+  const char* zrow = reinterpret_cast<const char*>(g_oae_zero_row) + (size_t)c0 * sizeof(T);
+  const int units16 = (int)(row_bytes >> 4);  // row_bytes % 16 == 0 (C = 32 * VEC, 16-B lanes)
 
   for (int p = threadIdx.x; p < a.P; p += blockDim.x)
     if (!anchor_keypoint(a.anchors + (int64_t)q * 10, p, a.offsets, 0.0f, s_kp + 3 * p))
@@ -243,8 +246,12 @@ __global__ void __launch_bounds__(kOaeWarps * 32, 2) oae_warp_kernel(OaeArgs a) 
       if (s < a.P * a.L) {
         const int t = cam * a.L + l;
         const double st = (double)a.strides[l];
-        s_rec[warp][s] = make_record((float)(u / st - 0.5), (float)(v / st - 0.5), a.start[t], a.shape[2 * t],
-                                     a.shape[2 * t + 1]);
+        SampleRec rec = make_record((float)(u / st - 0.5), (float)(v / st - 0.5), a.start[t], a.shape[2 * t],
+                                    a.shape[2 * t + 1]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)  // rows -> 16-B units: one shift per corner address in the load stream
+          rec.row[k] = rec.row[k] >= 0 ? rec.row[k] * units16 : -1;
+        s_rec[warp][s] = rec;
       }
     }
     __syncwarp();
@@ -291,10 +298,10 @@ __global__ void __launch_bounds__(kOaeWarps * 32, 2) oae_warp_kernel(OaeArgs a) 
             }
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              if (r[h][j].row[k] >= 0) c[h][j][k] = ld_row<NV>(feat + (size_t)r[h][j].row[k] * row_bytes);
-              else
-#pragma unroll
-                for (int i = 0; i < NV; ++i) c[h][j][k].v[i] = make_uint4(0, 0, 0, 0);
+              // out-of-grid corners read a static zero row (L1-resident): no
+              // predication or register zero-fill in the load stream
+              const int row = r[h][j].row[k];
+              c[h][j][k] = ld_row<NV>(row >= 0 ? feat + ((size_t)(uint32_t)row << 4) : zrow);
             }
           }
         }
@@ -523,7 +530,9 @@ int32_t msda_oae_pool(const msda_features_t* f, int32_t n_queries, const float* 
   cudaError_t e;
   const int C = f->channels;
   const bool al16 = al % 16 == 0;
-  const bool recs_fit = a.P * a.L <= kOaeMaxRecs;
+  // 16-B-unit row offsets in int32 (oae_warp_kernel): the table must stay below 32 GB
+  const bool recs_fit = a.P * a.L <= kOaeMaxRecs && (double)f->n_rows * f->channels * (f->dtype == MSDA_F32 ? 4 : 2) <
+                                                        (double)(1ll << 35);
   if (recs_fit && al16 && f->dtype == MSDA_F32 && C == 256) return launch_oae_warp<float, 8>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
   if (recs_fit && al16 && f->dtype == MSDA_F32 && C == 128) return launch_oae_warp<float, 4>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
   if (recs_fit && al16 && f->dtype == MSDA_F16 && C == 256) return launch_oae_warp<__half, 8>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
