@@ -187,13 +187,13 @@ def oae_case(reps, dev, cams=32, C=256, Q=900):
     K, R, T = ring(cams)
     camd = ops.Cameras(K, R, T, device=dev)
     anchors = anchors_for(Q, dev)
-    offs = (torch.rand((6, 3), generator=torch.Generator().manual_seed(3)) * 2 - 1)
+    offs = (torch.rand((6, 3), generator=torch.Generator().manual_seed(3)) * 2 - 1).to(dev)
+    strides = torch.tensor([4.0, 8.0, 16.0, 32.0], device=dev)  # resident: no per-call host copies
     g = torch.Generator(device=dev).manual_seed(4)
     desc = torch.randn((Q, C), generator=g, device=dev)
     vis = torch.rand((Q, cams), generator=g, device=dev)
     mem = torch.nn.functional.normalize(torch.randn((Q, C), generator=g, device=dev), dim=1)
-    fn = lambda: ops.oae_pool(feats, anchors, offs, camd, [4.0, 8.0, 16.0, 32.0], desc, vis, mem,  # noqa
-                              check=False)
+    fn = lambda: ops.oae_pool(feats, anchors, offs, camd, strides, desc, vis, mem, check=False)  # noqa: E731
     med, best = time_fn(fn, reps, flush=False)
     return {"config": "cfg4-oae", "path": "oae_pool (keypoint sampling + softmax + visibility fusion)",
             "dtype": "bfloat16", "cams": cams, "latency_us": med * 1e3, "best_us": best * 1e3,
