@@ -265,6 +265,28 @@ def normalize_groups(out, weight_sums, check=True):
     return out
 
 
+_CONST_CACHE: dict = {}
+
+
+def _small_const(values, dtype, dev, shape):
+    """Small per-call constants (level strides, learned keypoint offsets)
+    given as host lists/arrays: uploaded once per distinct value set and
+    device, then reused — a host→device copy from pageable memory would
+    synchronise every call.  Device tensors pass through untouched."""
+    if isinstance(values, torch.Tensor) and values.device == dev:
+        return values.to(dtype).reshape(shape).contiguous()
+    arr = np.ascontiguousarray(np.asarray(values.cpu() if isinstance(values, torch.Tensor) else values,
+                                          dtype=np.float64 if dtype == torch.float64 else np.float32))
+    key = (arr.tobytes(), arr.shape, str(dtype), str(dev))
+    hit = _CONST_CACHE.get(key)
+    if hit is None:
+        if len(_CONST_CACHE) > 256:
+            _CONST_CACHE.clear()
+        hit = torch.from_numpy(arr).to(device=dev, dtype=dtype).reshape(shape).contiguous()
+        _CONST_CACHE[key] = hit
+    return hit
+
+
 def msda_dense_project(feats: DeviceFeatures, anchors, learned_offsets, cameras: Cameras, strides, weights, dt=0.0,
                        precision="fast", normalize=False, out=None, check=False):
     """Dense MSDA with keypoint generation + projection fused into the kernel.
@@ -278,10 +300,10 @@ def msda_dense_project(feats: DeviceFeatures, anchors, learned_offsets, cameras:
     bs, q_n, ten = anchors.shape
     if ten != 10 or bs != feats.table.shape[0]:
         raise ValueError("anchors must be [bs, Q, 10] with bs == feature batch")
-    offs = torch.as_tensor(learned_offsets, dtype=torch.float32).reshape(-1, 3).to(dev).contiguous()
+    offs = _small_const(learned_offsets, torch.float32, dev, (-1, 3))
     n_learned = int(offs.shape[0])
     p_n = 7 + n_learned
-    strides = torch.as_tensor(strides, dtype=torch.float32).to(dev).contiguous()
+    strides = _small_const(strides, torch.float32, dev, (-1,))
     if strides.numel() != feats.n_levels:
         raise ValueError("one stride per level")
     wts = weights.to(device=dev, dtype=torch.float32).contiguous()
@@ -325,8 +347,8 @@ def oae_pool(feats: DeviceFeatures, anchors, learned_offsets, cameras: Cameras, 
     mem = memory.to(device=dev, dtype=torch.float32).contiguous()
     if tuple(vis.shape) != (q_n, feats.n_cams) or tuple(mem.shape) != (q_n, feats.channels):
         raise ValueError("visibility must be [Q, cams] and memory [Q, C]")
-    offs = torch.as_tensor(learned_offsets, dtype=torch.float32).reshape(-1, 3).to(dev).contiguous()
-    strides = torch.as_tensor(strides, dtype=torch.float32).to(dev).contiguous()
+    offs = _small_const(learned_offsets, torch.float32, dev, (-1, 3))
+    strides = _small_const(strides, torch.float32, dev, (-1,))
     out = torch.empty((q_n, feats.channels), dtype=torch.float32, device=dev)
     occl = torch.empty((q_n,), dtype=torch.uint8, device=dev)
     lib = L.lib()
