@@ -64,6 +64,30 @@ def precision_code(precision) -> int:
         raise ValueError(f"unknown precision mode: {precision!r}") from None
 
 
+_CONST_CACHE: dict = {}
+
+
+def _small_const(values, dtype, dev, shape):
+    """Small per-call constants (level strides, learned keypoint offsets)
+    given as host lists/arrays: uploaded once per distinct value set and
+    device, then reused — a host→device copy from pageable memory would
+    synchronise every call.  Device tensors pass through untouched."""
+    if isinstance(values, torch.Tensor) and values.device == dev:
+        return values.to(dtype).reshape(shape).contiguous()
+    np_dtype = {torch.float64: np.float64, torch.float32: np.float32, torch.int32: np.int32,
+                torch.int64: np.int64}[dtype]
+    arr = np.ascontiguousarray(np.asarray(values.cpu() if isinstance(values, torch.Tensor) else values,
+                                          dtype=np_dtype))
+    key = (arr.tobytes(), arr.shape, str(dtype), str(dev))
+    hit = _CONST_CACHE.get(key)
+    if hit is None:
+        if len(_CONST_CACHE) > 256:
+            _CONST_CACHE.clear()
+        hit = torch.from_numpy(arr).to(device=dev, dtype=dtype).reshape(shape).contiguous()
+        _CONST_CACHE[key] = hit
+    return hit
+
+
 @dataclass
 class DeviceFeatures:
     """Feature table resident in HBM.
@@ -86,8 +110,11 @@ class DeviceFeatures:
         if self.table.dtype not in _DTYPES:
             raise ValueError(f"unsupported feature dtype {self.table.dtype}")
         dev = self.table.device
-        self.spatial_shape = self.spatial_shape.to(device=dev, dtype=torch.int32).contiguous()
-        self.scale_start_index = self.scale_start_index.to(device=dev, dtype=torch.int64).contiguous()
+        # host-side shape tables (a per-call deformable_aggregation argument in
+        # Sparse4D) are uploaded once per value set, not copied every call
+        self.spatial_shape = _small_const(self.spatial_shape, torch.int32, dev, tuple(self.spatial_shape.shape))
+        self.scale_start_index = _small_const(self.scale_start_index, torch.int64, dev,
+                                              tuple(self.scale_start_index.shape))
         if self.spatial_shape.dim() != 3 or self.spatial_shape.shape[2] != 2:
             raise ValueError("spatial_shape must be [cams, levels, 2]")
         if tuple(self.scale_start_index.shape) != tuple(self.spatial_shape.shape[:2]):
@@ -263,28 +290,6 @@ def normalize_groups(out, weight_sums, check=True):
     code = L.lib().msda_dense_normalize(_ptr(out), _ptr(weight_sums), n_q, c_n, g_n, _ptr(ws), _stream(dev))
     _check_call(code, ws, dev, check, "normalize_groups")
     return out
-
-
-_CONST_CACHE: dict = {}
-
-
-def _small_const(values, dtype, dev, shape):
-    """Small per-call constants (level strides, learned keypoint offsets)
-    given as host lists/arrays: uploaded once per distinct value set and
-    device, then reused — a host→device copy from pageable memory would
-    synchronise every call.  Device tensors pass through untouched."""
-    if isinstance(values, torch.Tensor) and values.device == dev:
-        return values.to(dtype).reshape(shape).contiguous()
-    arr = np.ascontiguousarray(np.asarray(values.cpu() if isinstance(values, torch.Tensor) else values,
-                                          dtype=np.float64 if dtype == torch.float64 else np.float32))
-    key = (arr.tobytes(), arr.shape, str(dtype), str(dev))
-    hit = _CONST_CACHE.get(key)
-    if hit is None:
-        if len(_CONST_CACHE) > 256:
-            _CONST_CACHE.clear()
-        hit = torch.from_numpy(arr).to(device=dev, dtype=dtype).reshape(shape).contiguous()
-        _CONST_CACHE[key] = hit
-    return hit
 
 
 def msda_dense_project(feats: DeviceFeatures, anchors, learned_offsets, cameras: Cameras, strides, weights, dt=0.0,
