@@ -188,6 +188,69 @@ class _Contexts:
 _CONTEXTS = _Contexts()
 
 
+class _HostPins:
+    """Page-lock large host grids the caller passes again and again.
+
+    The reference API takes numpy arrays; from pageable memory every call
+    copies through the driver's staging buffers and the touched-row fetch
+    (which needs device-visible pages) cannot run.  A grid buffer seen in a
+    second call is registered (``msda_host_register``) for as long as its
+    owning array lives (``weakref.finalize`` unregisters it), so repeated
+    calls on the same pyramids — the reference bench, the decoder layers of
+    one frame — move their bytes at pinned-memory speed.  Buffers that cannot
+    be registered (already pinned, overlapping a registered page, not
+    weak-referenceable) are left alone.  ``MSDA_PIN_HOST=0`` disables it."""
+
+    MIN_BYTES = 4 << 20
+
+    def __init__(self):
+        import os
+
+        self.enabled = os.environ.get("MSDA_PIN_HOST", "1") != "0"
+        self._seen: dict = {}  # (ptr, nbytes) -> state: 1 seen once, 2 registered, 0 not registrable
+        self._lock = threading.Lock()
+
+    def note(self, arr):
+        if not self.enabled or arr.nbytes < self.MIN_BYTES:
+            return
+        import weakref
+
+        key = (arr.ctypes.data, arr.nbytes)
+        with self._lock:
+            state = self._seen.get(key)
+            if state is None:
+                self._seen[key] = 1
+                return
+            if state != 1:
+                return
+            owner = arr
+            while isinstance(owner.base, np.ndarray):
+                owner = owner.base
+            try:
+                ref = weakref.ref(owner)
+            except TypeError:
+                self._seen[key] = 0
+                return
+            del ref
+            if L.lib().msda_host_register(ctypes.c_void_p(key[0]), key[1], 0) != L.MSDA_OK:
+                self._seen[key] = 0
+                return
+            self._seen[key] = 2
+            weakref.finalize(owner, _HostPins._release, self, key)
+
+    @staticmethod
+    def _release(pins, key):
+        with pins._lock:
+            if pins._seen.pop(key, None) == 2:
+                try:
+                    L.lib().msda_host_unregister(ctypes.c_void_p(key[0]))
+                except Exception:  # interpreter shutdown: the driver releases it with the context
+                    pass
+
+
+_PINS = _HostPins()
+
+
 def last_h2d_bytes(device: int = 0) -> int:
     """Host->device bytes moved by the last host-buffer call on ``device``:
     whole grids copied plus the corner rows fetched from large, sparsely
@@ -272,6 +335,8 @@ def _run(pyramids, plan: SamplePlan, precision_code: int, normalize: bool, devic
             raise ValueError(f"plan references unknown camera id {plan.camera_ids[0]}")
         return np.zeros((q_n, 0), dtype=np.float32), np.diff(plan.offsets) == 0
     ids, n_levels, channels, cam_idx, ptrs, shape, keep = _prepare(pyr_map, plan, defer_range_check=True)
+    for g in keep:  # the grids' host buffers (page-locked once reused, see _HostPins)
+        _PINS.note(g)
     out = np.empty((q_n, channels), dtype=np.float32)
     empty = np.empty(q_n, dtype=np.uint8)
     cam_idx = np.ascontiguousarray(cam_idx, dtype=np.int32)

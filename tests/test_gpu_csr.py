@@ -294,3 +294,35 @@ def test_host_path_fetches_sparse_grids_from_pinned_memory(c_oracle, cuda_dev):
     out2, _ = F.msda_optimized(paged, plan)
     assert out2.tobytes() == ref.tobytes()
     assert F.last_h2d_bytes() >= table_bytes
+
+
+def test_reused_pageable_grids_get_page_locked(c_oracle, cuda_dev):
+    """Pageable numpy grids (the reference API's usual input): the first call
+    copies them whole; a grid buffer seen again is page-locked for as long as
+    its array lives, so from the second call on the sparse grids' touched rows
+    are fetched from it — same bytes out every time; released with the array."""
+    import gc
+
+    from paper_2601_10819_b200 import features as F
+    from paper_2601_10819_b200.workload import BenchWorkload, generate_workload
+
+    wl = BenchWorkload(cameras=2, levels=4, channels=64, queries=60, points_per_query=13, level0_size=(180, 320))
+    gw = generate_workload(wl)
+    pyrs, plan = _gw_pyramids(F, gw)
+    paged = [F.FeaturePyramid(p.camera_id, [F.FeatureGrid(stride=g.stride, values=np.array(g.values))
+                                            for g in p.levels]) for p in pyrs]
+    ref, _ = c_oracle.msda_c(gw.table, gw.tiles, wl.levels, gw.offsets, gw.camera_ids, gw.levels, gw.us, gw.vs,
+                             gw.weights)
+    moved = []
+    for _ in range(3):
+        out, _ = F.msda_optimized(paged, plan)
+        assert out.tobytes() == ref.tobytes()
+        moved.append(F.last_h2d_bytes())
+    assert moved[0] >= gw.table.nbytes  # first sighting: copied whole
+    assert moved[1] < 0.6 * gw.table.nbytes and moved[2] == moved[1]  # level 0 fetched row by row
+    big = [(g.values.ctypes.data, g.values.nbytes) for p in paged for g in p.levels
+           if g.values.nbytes >= F._PINS.MIN_BYTES]
+    assert big and all(F._PINS._seen.get(k) == 2 for k in big)
+    del paged, pyrs, out
+    gc.collect()
+    assert not any(k in F._PINS._seen for k in big)  # unregistered with their arrays
