@@ -331,3 +331,38 @@ def test_reused_pageable_grids_get_page_locked(c_oracle, cuda_dev):
     # gc.collect(); the release itself is exercised either way)
     if "NV_SANITIZER_INJECTION_TRANSPORT_TYPE" not in os.environ:
         assert not any(k in F._PINS._seen for k in big)  # unregistered with their arrays
+
+
+def test_exact_path_replays_in_a_cuda_graph(c_oracle, cuda_dev):
+    """The exact CSR call (status reset, canonicaliser, programmatically
+    launched gather) captured once in a CUDA graph and replayed: same bytes as
+    the eager call and the oracle on every replay, inputs updated in place
+    between replays (the decoder-layer pattern)."""
+    import torch
+
+    from paper_2601_10819_b200 import ops
+    from paper_2601_10819_b200.workload import BenchWorkload, generate_workload
+
+    wl = BenchWorkload(cameras=3, levels=4, channels=128, queries=200, points_per_query=13, level0_size=(64, 176))
+    gw = generate_workload(wl)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(cuda_dev)  # noqa: E731
+    feats = ops.DeviceFeatures(t(gw.table), t(gw.spatial_shape), t(gw.tile_start.reshape(wl.cameras, wl.levels)))
+    plan = [t(gw.offsets), t(gw.camera_ids), t(gw.levels), t(gw.us), t(gw.vs), t(gw.weights)]
+    out = torch.empty((wl.queries, wl.channels), device=cuda_dev)
+    empty = torch.empty((wl.queries,), dtype=torch.uint8, device=cuda_dev)
+    ops.msda_csr(feats, *plan, out=out, empty=empty, check=True)  # warm-up: workspace + attributes
+    s = torch.cuda.Stream(cuda_dev)
+    s.wait_stream(torch.cuda.current_stream(cuda_dev))
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        ops.msda_csr(feats, *plan, out=out, empty=empty, check=False)
+    rng = np.random.default_rng(8)
+    for rep in range(3):
+        w = gw.weights if rep == 0 else rng.uniform(0.01, 1.0, gw.weights.shape).astype(np.float32)
+        plan[5].copy_(t(w))
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize(cuda_dev)
+        ref, _ = c_oracle.msda_c(gw.table, gw.tiles, wl.levels, gw.offsets, gw.camera_ids, gw.levels, gw.us, gw.vs,
+                                 w)
+        assert out.cpu().numpy().tobytes() == ref.tobytes(), rep
