@@ -503,7 +503,8 @@ def run_ours(args, cfg, rank, local_rank, world):
 DENSE_CONFIGS = {
     # cfg5 (BASELINE configs[4]): 512 cameras of the cfg1 per-camera shape, fp16, Sparse4D dense FAST path
     "cfg5-stream": dict(cams=512, scene=32, shard="stream",
-                        desc="512 cams as 16 scenes x 32 cams, fp16, dense FAST, scenes dealt round-robin to ranks"),
+                        desc="512 cams as 16 scenes x 32 cams, fp16, dense FAST, scenes dealt round-robin to ranks, "
+                             "each rank's scenes aggregated as one batched call"),
     "cfg5-camera-peer": dict(cams=512, scene=512, shard="camera", transport="peer",
                              desc="one 512-cam scene, fp16, dense FAST, cameras split across ranks, partials pushed "
                                   "into every rank's buffer over NVLink (CUDA IPC, peer.cu) instead of NCCL"),
@@ -543,12 +544,23 @@ def run_dense_scaling(args, cfg, rank, local_rank, world):
         return loc, w.reshape(1, Q, P, n_cams, L, G).contiguous()
 
     if cfg["shard"] == "stream":
+        # this rank's scenes as ONE batched call: the scenes share the camera
+        # and level geometry, so their tables stack as batch items [S, R, C]
+        # (one launch fills the GPU; 16 sequential per-scene calls measured
+        # 4.40 ms vs the batch below)
         mine = shard_streams(cfg["cams"] // cfg["scene"], rank, world)
-        work = [(scene_feats(cfg["scene"]), *inputs(cfg["scene"])) for _ in mine]
+        scenes = [scene_feats(cfg["scene"]) for _ in mine]
+        ins = [inputs(cfg["scene"]) for _ in mine]
+        if scenes:
+            feats = ops.DeviceFeatures(torch.cat([f.table for f in scenes], 0), scenes[0].spatial_shape,
+                                       scenes[0].scale_start_index)
+            loc = torch.cat([x[0] for x in ins], 0)
+            w = torch.cat([x[1] for x in ins], 0)
+            del scenes, ins
 
         def step():
-            for f, loc, w in work:
-                ops.deformable_aggregation(f, None, None, loc, w, precision="fast")
+            if mine:
+                ops.deformable_aggregation(feats, None, None, loc, w, precision="fast")
     else:
         lo, hi = camera_range(cfg["cams"], rank, world)
         feats = scene_feats(hi - lo)
