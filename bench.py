@@ -494,6 +494,12 @@ def run_ours(args, cfg, rank, local_rank, world):
                        else f"{nq} of {wl.queries} queries x3 reps (1 warm-up), extrapolated linearly"),
             "algorithm": "oracle msda_tiled (reference msda_optimized FULL restated, numpy, threads)",
             "gpu_bitwise_equal_on_sample": bool(parity)}
+        # SURVEY §8(d) also asks for the single-thread figure (msda_optimized, workers=1): one bounded rep
+        r1 = cpu_reference_time(gw, budget_s=12.0, reps=1, workers=1)
+        line["cpu_baseline"]["single_thread"] = {
+            "value": wl.cameras / r1["full_call_s"], "unit": "camera-frames/s", "cores": 1,
+            "sample": (f"full workload x1 rep after 1 warm-up" if r1["sample_queries"] == wl.queries
+                       else f"{r1['sample_queries']} of {wl.queries} queries x1 rep, extrapolated linearly")}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
