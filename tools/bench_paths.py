@@ -327,6 +327,8 @@ def main():
                                    torch.float16, "fast", args.reps, dev),
         "cfg3_h2": lambda: dense_case("cfg3 64 cams fp16, half2 accumulation", 64, CFG1_LEVELS, 256, 8,
                                       torch.float16, "fast_h2", args.reps, dev),
+        "cfg3_exact": lambda: dense_case("cfg3 64 cams fp16, exact (bit-faithful f32 arithmetic)", 64, CFG1_LEVELS,
+                                         256, 8, torch.float16, "exact", max(3, args.reps // 4), dev),
         "cfg4d": lambda: dense_case("cfg4 MSDA part: 32 cams bf16", 32, CFG1_LEVELS, 256, 8, torch.bfloat16, "fast",
                                     args.reps, dev),
         "cfg5": lambda: dense_case("cfg5 512 cams fp16 (1 GPU)", 512, CFG1_LEVELS, 256, 8, torch.float16, "fast",
