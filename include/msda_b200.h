@@ -236,7 +236,8 @@ int32_t msda_assoc_cost(const double *q_centers, const double *d_centers, const 
                         uint8_t *admissible, void *stream);
 
 /* Data-dependent status of the last call that used `workspace` (synchronises
- * `stream`).  detail = offending query / sample index, or -1.               */
+ * `stream`).  detail = the smallest offending query / sample index reported
+ * for the winning status code (the reference names the first), or -1.      */
 int32_t msda_read_status(const void *workspace, void *stream, int32_t *status, int64_t *detail);
 
 /* ---- host-buffer entry point (end-to-end, copies inside the call) ---- */
@@ -253,11 +254,26 @@ int32_t msda_csr_host(msda_context_t *ctx, const void *const *level_data, const 
                       const int32_t *level, const float *u, const float *v, const float *weight,
                       int32_t precision, int32_t normalize, float *out, uint8_t *empty);
 
+/* bilinear_sample (features.py:184-219) over HOST buffers, on the device:
+ * grid (H, W, C) f32 row-major, n cell coordinates u, v (finite; the caller
+ * raises for non-finite ones as the reference does), out [n, C] f32 =
+ * (c00*w00 + c10*w10) + (c01*w01 + c11*w11) with out-of-grid neighbours
+ * reading zero — bit-identical to the reference.  A page-locked grid is read
+ * in place; a pageable one is copied.  Synchronous.                         */
+int32_t msda_bilinear_host(msda_context_t *ctx, const float *grid, int32_t H, int32_t W, int32_t C, int64_t n,
+                           const float *u, const float *v, float *out);
+
 /* Host->device bytes the last msda_csr_host call moved: whole grids copied
  * plus, for large sparsely sampled grids in pinned (device-visible) host
  * memory, only the corner rows the plan touches (fetched over PCIe by the
  * device, once each).                                                       */
 long long msda_context_last_h2d_bytes(const msda_context_t *ctx);
+
+/* Offending query (zero weight sum, malformed CSR offsets) or sample (unknown
+ * target, non-finite value) of the last msda_csr_host call's non-OK status:
+ * the smallest such index, as the reference's sequential loop reports the
+ * first (features.py:264-269); -1 when none.                                */
+long long msda_context_last_detail(const msda_context_t *ctx);
 
 #ifdef __cplusplus
 }

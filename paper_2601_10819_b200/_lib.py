@@ -75,6 +75,8 @@ SIGNATURES = {
     "msda_context_create": (I32, [I32, ctypes.POINTER(P)]),
     "msda_context_destroy": (None, [P]),
     "msda_context_last_h2d_bytes": (ctypes.c_longlong, [P]),
+    "msda_context_last_detail": (ctypes.c_longlong, [P]),
+    "msda_bilinear_host": (I32, [P, P, I32, I32, I32, I64, P, P, P]),
     "msda_csr_host": (I32, [P, P, P, I32, I32, I32, I32, I64, P, P, P, P, P, P, I32, I32, P, P]),
     "msda_host_register": (I32, [P, SZ, I32]),
     "msda_host_unregister": (I32, [P]),

@@ -79,6 +79,28 @@ __global__ void __launch_bounds__(256) fetch_rows_kernel(FetchArgs a) {
   }
 }
 
+// bilinear_sample (features.py:184-219) for n (u, v) cell coordinates on one
+// (H, W, C) grid: one warp per sample, the reference's f32 tree
+// ((c00*w00 + c10*w10) + (c01*w01 + c11*w11)), each product and sum rounded
+// once, out-of-grid corners read as +0 rows.  `grid` is device memory or a
+// device-visible pinned host buffer.
+__global__ void bilinear_kernel(const float* __restrict__ grid, int H, int W, int C, const float* __restrict__ u,
+                                const float* __restrict__ v, int64_t n, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n;
+       i += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const SampleRec r = make_record(u[i], v[i], 0, H, W);
+    for (int c = lane; c < C; c += 32) {
+      float cv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cv[k] = r.row[k] >= 0 ? grid[(size_t)r.row[k] * C + c] : 0.0f;
+      const float a = __fadd_rn(__fmul_rn(cv[0], r.iw[0]), __fmul_rn(cv[1], r.iw[1]));
+      const float b = __fadd_rn(__fmul_rn(cv[2], r.iw[2]), __fmul_rn(cv[3], r.iw[3]));
+      out[i * C + c] = __fadd_rn(a, b);
+    }
+  }
+}
+
 cudaError_t launch_f32_to_f16(const float* src, __half* dst, int64_t n, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 32);
@@ -192,7 +214,7 @@ int32_t msda_read_status(const void* workspace, void* stream_, int32_t* status, 
     return MSDA_CUDA_ERROR;
   if (cudaStreamSynchronize(stream) != cudaSuccess) return MSDA_CUDA_ERROR;
   if (status) *status = h.code;
-  if (detail) *detail = h.code ? h.detail : -1;
+  if (detail) *detail = status_detail(h);
   return MSDA_OK;
 }
 
@@ -207,7 +229,10 @@ struct msda_context {
   void* arena = nullptr;
   size_t arena_bytes = 0;
   long long last_h2d_bytes = 0;  // host->device bytes moved by the last msda_csr_host call
+  long long last_detail = -1;    // offending query / sample of the last call's status, or -1
 };
+
+long long msda_context_last_detail(const msda_context_t* ctx) { return ctx ? ctx->last_detail : -1; }
 
 long long msda_context_last_h2d_bytes(const msda_context_t* ctx) { return ctx ? ctx->last_h2d_bytes : -1; }
 
@@ -286,6 +311,15 @@ int32_t msda_csr_host(msda_context_t* ctx, const void* const* level_data, const 
   if (channels % 2) return MSDA_ODD_CHANNELS;
   if (dtype < MSDA_F32 || dtype > MSDA_BF16) return MSDA_BAD_ARG;
   if (cudaSetDevice(ctx->device) != cudaSuccess) return MSDA_CUDA_ERROR;
+  ctx->last_detail = -1;
+  // CSR offsets (HOST): offsets[0] == 0 and non-decreasing, else the plan
+  // arrays' extent (offsets[n_queries] samples) is not what the caller holds
+  if (offsets[0] != 0) return MSDA_BAD_ARG;
+  for (int64_t q = 0; q < n_queries; ++q)
+    if (offsets[q + 1] < offsets[q]) {
+      ctx->last_detail = q;
+      return MSDA_BAD_ARG;
+    }
   const size_t esz = dtype == MSDA_F32 ? 4 : 2;
   const int n_tiles = n_cams * n_levels;
   std::vector<int64_t> start(n_tiles);
@@ -397,10 +431,17 @@ int32_t msda_csr_host(msda_context_t* ctx, const void* const* level_data, const 
     cudaStreamSynchronize(ctx->copy_stream);
     return MSDA_CUDA_ERROR;
   }
+  // every return from here on first drains both streams: the caller's host
+  // buffers may still be the source of in-flight DMAs
+  auto fail = [&](int32_t code) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamSynchronize(s);
+    return code;
+  };
   if (cvt_half) {
     if (launch_f32_to_f16(reinterpret_cast<const float*>(d_tab), reinterpret_cast<__half*>(d_half),
                           rows * (int64_t)channels, s) != cudaSuccess)
-      return MSDA_CUDA_ERROR;
+      return fail(MSDA_CUDA_ERROR);
   }
   msda_features_t f{};
   f.data = cvt_half ? d_half : d_tab;
@@ -414,22 +455,70 @@ int32_t msda_csr_host(msda_context_t* ctx, const void* const* level_data, const 
   f.scale_start_index = d_start;
   msda_csr_plan_t pl{n_queries, S, d_off, d_cam, d_lvl, d_u, d_v, d_w};
   st = msda_csr(&f, &pl, precision, normalize, d_out, d_emp, d_ws, ws_b, s);
-  if (st != MSDA_OK) return st;
+  if (st != MSDA_OK) return fail(st);
   if (cudaMemcpyAsync(out, d_out, (size_t)n_queries * channels * 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-    return MSDA_CUDA_ERROR;
+    return fail(MSDA_CUDA_ERROR);
   if (empty && cudaMemcpyAsync(empty, d_emp, (size_t)n_queries, cudaMemcpyDeviceToHost, s) != cudaSuccess)
-    return MSDA_CUDA_ERROR;
+    return fail(MSDA_CUDA_ERROR);
   int32_t dev_status = 0;
-  int64_t detail = 0;
+  int64_t detail = -1;
   st = msda_read_status(d_ws, s, &dev_status, &detail);  // synchronises the stream
-  if (st != MSDA_OK) return st;
+  if (st != MSDA_OK) return fail(st);
+  ctx->last_detail = detail;
   if (any_fetch) {
     unsigned long long rows_fetched = 0;
-    if (cudaMemcpy(&rows_fetched, d_fetched, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return MSDA_CUDA_ERROR;
+    if (cudaMemcpy(&rows_fetched, d_fetched, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return fail(MSDA_CUDA_ERROR);
     h2d += (long long)(rows_fetched * channels * esz);
   }
   ctx->last_h2d_bytes = h2d;
   return dev_status;
+}
+
+
+// bilinear_sample over HOST buffers: grid (H, W, C) f32, n coordinates, out
+// [n, C].  A page-locked grid is read in place by the kernel (only the corner
+// rows cross PCIe); a pageable one is copied whole into the context arena.
+int32_t msda_bilinear_host(msda_context_t* ctx, const float* grid, int32_t H, int32_t W, int32_t C, int64_t n,
+                           const float* u, const float* v, float* out) {
+  if (!ctx || !grid || H <= 0 || W <= 0 || C <= 0 || n < 0 || (n > 0 && (!u || !v || !out))) return MSDA_BAD_ARG;
+  if ((int64_t)H * W >= (int64_t(1) << 31)) return MSDA_BAD_ARG;
+  if (cudaSetDevice(ctx->device) != cudaSuccess) return MSDA_CUDA_ERROR;
+  ctx->last_detail = -1;
+  if (n == 0) return MSDA_OK;
+  const size_t grid_b = (size_t)H * W * C * 4;
+  const float* d_grid = nullptr;
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, grid) == cudaSuccess && pa.type == cudaMemoryTypeHost && pa.devicePointer)
+    d_grid = reinterpret_cast<const float*>(pa.devicePointer);
+  else
+    cudaGetLastError();
+  const size_t gb = d_grid ? 0 : align_up(grid_b, 256), cb = align_up((size_t)n * 4, 256);
+  const size_t ob = align_up((size_t)n * C * 4, 256);
+  int32_t st = ctx_reserve(ctx, gb + 2 * cb + ob);
+  if (st != MSDA_OK) return st;
+  char* p = reinterpret_cast<char*>(ctx->arena);
+  cudaStream_t s = ctx->stream;
+  long long h2d = 2 * n * 4;
+  bool ok = true;
+  if (!d_grid) {
+    ok = cudaMemcpyAsync(p, grid, grid_b, cudaMemcpyHostToDevice, s) == cudaSuccess;
+    d_grid = reinterpret_cast<const float*>(p);
+    h2d += (long long)grid_b;
+  }
+  float* d_u = reinterpret_cast<float*>(p + gb);
+  float* d_v = reinterpret_cast<float*>(p + gb + cb);
+  float* d_out = reinterpret_cast<float*>(p + gb + 2 * cb);
+  ok = ok && cudaMemcpyAsync(d_u, u, (size_t)n * 4, cudaMemcpyHostToDevice, s) == cudaSuccess;
+  ok = ok && cudaMemcpyAsync(d_v, v, (size_t)n * 4, cudaMemcpyHostToDevice, s) == cudaSuccess;
+  if (ok) {
+    const int64_t blocks = std::min<int64_t>((n + 7) / 8, (int64_t)num_sms_for_current_device() * 16);
+    bilinear_kernel<<<(unsigned)blocks, 256, 0, s>>>(d_grid, H, W, C, d_u, d_v, n, d_out);
+    ok = cudaGetLastError() == cudaSuccess;
+  }
+  ok = ok && cudaMemcpyAsync(out, d_out, (size_t)n * C * 4, cudaMemcpyDeviceToHost, s) == cudaSuccess;
+  const bool synced = cudaStreamSynchronize(s) == cudaSuccess;
+  ctx->last_h2d_bytes = h2d;
+  return ok && synced ? MSDA_OK : MSDA_CUDA_ERROR;
 }
 
 }  // extern "C"

@@ -21,16 +21,24 @@ struct __align__(16) SampleRec {
   float iw[4];
 };
 
-// Device status word at the head of every workspace.
+// Device status word at the head of every workspace (zeroed before a call).
+// The first error code wins; among reports of that code the smallest detail
+// (query / sample index) is kept, so the message names the first offending
+// query as the reference's sequential loop does (features.py:264-269).
+// detail_enc holds ~detail (0 = none) so that atomicMax keeps the minimum.
 struct DevStatus {
   int32_t code;
   int32_t pad;
-  long long detail;
+  unsigned long long detail_enc;
 };
 constexpr size_t kStatusBytes = 256;
 
 __device__ __forceinline__ void set_status(DevStatus* st, int code, long long detail) {
-  if (atomicCAS(&st->code, 0, code) == 0) st->detail = detail;
+  const int prev = atomicCAS(&st->code, 0, code);
+  if ((prev == 0 || prev == code) && detail >= 0) atomicMax(&st->detail_enc, ~(unsigned long long)detail);
+}
+__host__ __device__ inline long long status_detail(const DevStatus& st) {
+  return (st.code && st.detail_enc) ? (long long)~st.detail_enc : -1;
 }
 
 // Order-preserving float -> uint32 map (ascending float order == ascending

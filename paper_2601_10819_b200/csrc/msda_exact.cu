@@ -62,6 +62,7 @@ struct PlanArgs {
   const float* v;
   const float* w;
   int64_t n_queries;
+  int64_t n_samples;  // offsets must satisfy 0 <= offsets[q] <= offsets[q + 1] <= n_samples
   int32_t n_cams, n_levels;
   const int32_t* shape;
   const int64_t* start;
@@ -158,6 +159,10 @@ __global__ void __launch_bounds__(kPlanThreads) plan_canon_kernel(PlanArgs a) {
 
   for (int64_t q = blockIdx.x; q < a.n_queries; q += gridDim.x) {
     const int64_t lo = a.offsets[q], hi = a.offsets[q + 1];
+    if (lo < 0 || hi < lo || hi > a.n_samples) {  // malformed CSR offsets: report, touch nothing
+      if (threadIdx.x == 0) set_status(a.status, MSDA_BAD_ARG, q);
+      continue;
+    }
     const int n = (int)(hi - lo);
     if (n <= 0) continue;
     // two inlined copies so the shared-memory one compiles to LDS/STS (a
@@ -298,6 +303,7 @@ struct GatherArgs {
   int32_t c_off;       // first channel of the slice
   int32_t out_stride;  // floats per output row
   int64_t n_queries;
+  int64_t n_samples;  // CSR offsets are clamped to [0, n_samples] (the plan kernel reports bad ones)
   const int64_t* offsets;
   const SampleRec* rec;
   const float* wn;
@@ -388,12 +394,14 @@ __device__ __forceinline__ void half_accumulate(__half2* acch, const void* const
 template <typename T, int VEC, bool HALF, int UNROLL>
 __global__ void __launch_bounds__(256) gather_exact_kernel(GatherArgs a) {
   constexpr int BYTES = VEC * (int)sizeof(T);
+  if (a.status && *reinterpret_cast<volatile const int32_t*>(&a.status->code) == MSDA_BAD_ARG) return;
   const int lanes_per_q = a.C / VEC;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t q = gtid / lanes_per_q;
   if (q >= a.n_queries) return;
   const int c0 = (int)(gtid - q * lanes_per_q) * VEC;
-  const int64_t lo = a.offsets[q], hi = a.offsets[q + 1];
+  const int64_t lo = min(max(a.offsets[q], (int64_t)0), a.n_samples);
+  const int64_t hi = min(max(a.offsets[q + 1], lo), a.n_samples);
   const char* feat = reinterpret_cast<const char*>(a.feat) + (size_t)(a.c_off + c0) * sizeof(T);
   const size_t row_bytes = (size_t)a.row_elems * sizeof(T);
 
@@ -534,6 +542,9 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   // and sums are visible once the primary grid has completed (a no-op when
   // launched normally)
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // malformed CSR offsets (reported by the plan kernel): the workspace
+  // records are not all written, read none of them
+  if (!RAW && a.status && *reinterpret_cast<volatile const int32_t*>(&a.status->code) == MSDA_BAD_ARG) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* base = smem_raw + warp * SM::kPerWarp;
   int4* s_rows = reinterpret_cast<int4*>(base + SM::kCorner);
@@ -557,8 +568,8 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   if (q >= a.n_queries) return;
   const int c0 = (int)(gw - q * warps_per_q) * 32 * VEC + lane * VEC;
   const int nd = DENSE ? a.P * n_cam * a.n_levels : 0;  // samples of this dense split
-  const int64_t lo = DENSE ? 0 : a.offsets[q];
-  const int n = DENSE ? nd : (int)(a.offsets[q + 1] - lo);
+  const int64_t lo = DENSE ? 0 : min(max(a.offsets[q], (int64_t)0), a.n_samples);
+  const int n = DENSE ? nd : (int)(min(max(a.offsets[q + 1], lo), a.n_samples) - lo);
   const SampleRec* rec = a.rec + lo;
   const float* wnp = a.wn + lo * (GW > 1 ? a.n_groups : 1);
   const int gl = GW > 1 ? (a.c_off + c0) / a.cpg : 0;  // this lane's channel group
@@ -570,6 +581,9 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   float wsum = 1.0f;
   float wsum_g = 0.0f;  // DENSE: this lane's group weight sum
   if constexpr (RAW && !DENSE) {
+    // no plan kernel runs in FAST: the gather reports malformed offsets itself
+    if (head && lane == 0 && (a.offsets[q] < 0 || a.offsets[q + 1] < a.offsets[q] || a.offsets[q + 1] > a.n_samples))
+      set_status(a.status, MSDA_BAD_ARG, q);
     if (a.normalize) {  // per-query weight sum, any order (FAST)
       float t = 0.0f;
       for (int s = lane; s < n; s += 32) t += __ldg(a.w + lo + s);
@@ -1015,6 +1029,7 @@ cudaError_t launch_plan_canon(const msda_features_t& f, const msda_csr_plan_t& p
   a.v = p.v;
   a.w = p.weight;
   a.n_queries = p.n_queries;
+  a.n_samples = p.n_samples;
   a.n_cams = f.n_cams;
   a.n_levels = f.n_levels;
   a.shape = f.spatial_shape;
@@ -1052,6 +1067,7 @@ cudaError_t launch_gather_exact(const msda_features_t& f, const msda_csr_plan_t&
   g.c_off = c_off;
   g.out_stride = f.channels;
   g.n_queries = p.n_queries;
+  g.n_samples = p.n_samples;
   g.offsets = p.offsets;
   g.rec = w.rec;
   g.wn = w.wn;

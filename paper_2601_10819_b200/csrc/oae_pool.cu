@@ -531,7 +531,8 @@ int32_t msda_oae_pool(const msda_features_t* f, int32_t n_queries, const float* 
   const int C = f->channels;
   const bool al16 = al % 16 == 0;
   // 16-B-unit row offsets in int32 (oae_warp_kernel): the table must stay below 32 GB
-  const bool recs_fit = a.P * a.L <= kOaeMaxRecs && (double)f->n_rows * f->channels * (f->dtype == MSDA_F32 ? 4 : 2) <
+  // the warp kernel projects one keypoint per lane (32-bit ballot): P <= 32
+  const bool recs_fit = a.P <= 32 && a.P * a.L <= kOaeMaxRecs && (double)f->n_rows * f->channels * (f->dtype == MSDA_F32 ? 4 : 2) <
                                                         (double)(1ll << 35);
   if (recs_fit && al16 && f->dtype == MSDA_F32 && C == 256) return launch_oae_warp<float, 8>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
   if (recs_fit && al16 && f->dtype == MSDA_F32 && C == 128) return launch_oae_warp<float, 4>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;

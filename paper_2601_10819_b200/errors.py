@@ -35,6 +35,22 @@ class AllOccluded(Exception):
                          "caller should fall back to the query's memory embedding")
 
 
+# When the reference package is importable, raise ITS classes, so callers'
+# ``except mvtrack3d.errors.NonFiniteWeight`` clauses catch the drop-in's
+# errors too (the classes above are the same taxonomy, errors.py:10-46).
+try:  # pragma: no cover - depends on the environment
+    from mvtrack3d import errors as _ref_errors
+except Exception:  # the reference is not installed: keep the local classes
+    _ref_errors = None
+if _ref_errors is not None:
+    BehindCamera = _ref_errors.BehindCamera  # noqa: F811
+    OffsetOutOfRange = _ref_errors.OffsetOutOfRange  # noqa: F811
+    NonFiniteWeight = _ref_errors.NonFiniteWeight  # noqa: F811
+    OddChannelCount = _ref_errors.OddChannelCount  # noqa: F811
+    ChannelMismatch = _ref_errors.ChannelMismatch  # noqa: F811
+    AllOccluded = _ref_errors.AllOccluded  # noqa: F811
+
+
 class MsdaCudaError(RuntimeError):
     """The CUDA runtime reported a failure inside the C-ABI library."""
 
@@ -59,7 +75,7 @@ def raise_for_status(code: int, detail: int = -1, what: str = "") -> None:
     exc = _BY_CODE.get(int(code), RuntimeError)
     msg = L.status_string(code)
     if detail is not None and detail >= 0:
-        unit = "query" if code == L.MSDA_ZERO_WEIGHT_SUM else "sample"
+        unit = "query" if code in (L.MSDA_ZERO_WEIGHT_SUM, L.MSDA_BAD_ARG) else "sample"
         msg = f"{unit} {detail}: {msg}"
     if what:
         msg = f"{what}: {msg}"

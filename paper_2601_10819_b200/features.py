@@ -3,9 +3,12 @@
 Same names, argument meaning and error behaviour as
 ``/root/reference/pkg/src/mvtrack3d/features.py`` — ``FeatureGrid``,
 ``FeaturePyramid``, ``SamplePlan``, ``PrecisionMode``, ``pixel_to_cell``,
-``cell_to_pixel``, ``msda_reference``, ``msda_optimized`` — but the
-aggregation runs on the GPU through the C ABI (``msda_csr_host``: host
-arrays in, host arrays out, copies inside the call).
+``cell_to_pixel``, ``bilinear_sample``, ``msda_reference``,
+``msda_optimized`` — but the arithmetic runs on the GPU through the C ABI
+(``msda_csr_host`` / ``msda_bilinear_host``: host arrays in, host arrays out,
+copies inside the call).  The reference's own ``FeatureGrid`` /
+``FeaturePyramid`` / ``SamplePlan`` objects are accepted too (the calls read
+only their attributes).
 
 ``msda_optimized(FULL)`` and ``msda_reference`` are bit-identical to the
 reference's (canonical per-query order, same f32 expression tree);
@@ -129,11 +132,21 @@ class SamplePlan:
 
     @classmethod
     def from_csr(cls, offsets, camera_ids, levels, us, vs, weights):
-        """Adopt CSR arrays as-is (no copy when dtypes already match)."""
+        """Adopt CSR arrays as-is (no copy when dtypes already match).
+
+        ``offsets`` must start at 0, never decrease and end at the sample
+        count every per-sample array holds (the ``SamplePlan`` invariant the
+        reference's constructors establish, features.py:122-171)."""
         plan = cls.__new__(cls)
-        plan._finalize(np.ascontiguousarray(offsets, dtype=np.int64), np.ascontiguousarray(camera_ids, np.int32),
-                       np.ascontiguousarray(levels, np.int32), np.ascontiguousarray(us, np.float32),
-                       np.ascontiguousarray(vs, np.float32), np.ascontiguousarray(weights, np.float32))
+        offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+        cols = [np.ascontiguousarray(camera_ids, np.int32), np.ascontiguousarray(levels, np.int32),
+                np.ascontiguousarray(us, np.float32), np.ascontiguousarray(vs, np.float32),
+                np.ascontiguousarray(weights, np.float32)]
+        if offsets.ndim != 1 or offsets.size == 0 or offsets[0] != 0 or np.any(np.diff(offsets) < 0):
+            raise ValueError("offsets must start at 0 and be non-decreasing")
+        if any(c.ndim != 1 or c.size != offsets[-1] for c in cols):
+            raise ValueError(f"plan arrays must hold offsets[-1] = {int(offsets[-1])} samples")
+        plan._finalize(offsets, *cols)
         return plan
 
     def _finalize(self, offsets, cam, lvl, us, vs, ws):
@@ -345,11 +358,36 @@ def _run(pyramids, plan: SamplePlan, precision_code: int, normalize: bool, devic
             _CONTEXTS.get(device), ptrs, _ptr(shape), len(ids), n_levels, channels, L.MSDA_F32, q_n,
             _ptr(plan.offsets), _ptr(cam_idx), _ptr(plan.levels), _ptr(plan.us), _ptr(plan.vs),
             _ptr(plan.weights), precision_code, int(bool(normalize)), _ptr(out), _ptr(empty))
+        detail = int(L.lib().msda_context_last_detail(_CONTEXTS.get(device))) if code != L.MSDA_OK else -1
     del keep
     if code != L.MSDA_OK:
         _prepare(pyr_map, plan)  # a bad target outranks every other error, worded as the reference does
-    raise_for_status(code, -1, "msda")
+    # zero weight sum: "query {q}: plan weights sum to zero, cannot renormalize"
+    # with the first offending q (features.py:269 / 287)
+    raise_for_status(code, detail)
     return out, empty.astype(bool)
+
+
+def bilinear_sample(pyramid, level: int, u: float, v: float, device: int = 0) -> np.ndarray:
+    """Bilinearly interpolate one level at cell coordinates (u, v) (features.py:184-219).
+
+    Cell centres at integers; neighbours outside [0, W-1] x [0, H-1] read
+    zero.  Returns a (C,) float32 vector, bit-identical to the reference's,
+    computed on the GPU (C ABI ``msda_bilinear_host``)."""
+    if not (np.isfinite(u) and np.isfinite(v)):
+        raise ValueError("sample coordinates must be finite")
+    vals = pyramid.levels[level].values
+    height, width, channels = vals.shape
+    _PINS.note(vals)
+    out = np.empty((1, channels), dtype=np.float32)
+    uu = np.array([u], dtype=np.float32)
+    vv = np.array([v], dtype=np.float32)
+    grid = np.ascontiguousarray(vals, dtype=np.float32)
+    with _CONTEXTS.call_lock(device):
+        code = L.lib().msda_bilinear_host(_CONTEXTS.get(device), _ptr(grid), height, width, channels, 1, _ptr(uu),
+                                          _ptr(vv), _ptr(out))
+    raise_for_status(code, -1, "bilinear_sample")
+    return out[0]
 
 
 def msda_reference(pyramids, plan: SamplePlan, normalize: bool = True, device: int = 0):

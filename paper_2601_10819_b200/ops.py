@@ -265,6 +265,8 @@ def deformable_aggregation_partial(feats: DeviceFeatures, sampling_location, wei
     if tuple(loc.shape) != (bs, q_n, p_n, feats.n_cams, 2) or tuple(wts.shape) != (
             bs, q_n, p_n, feats.n_cams, feats.n_levels, g_n):
         raise ValueError("sampling_location [bs, Q, P, cams, 2] and weights [bs, Q, P, cams, L, G] expected")
+    if bs != feats.table.shape[0]:  # the C ABI takes the batch from the feature descriptor
+        raise ValueError("batch of the feature table and sampling_location differ")
     out = torch.empty((bs, q_n, feats.channels), dtype=torch.float32, device=dev)
     wsum = torch.empty((bs, q_n, g_n), dtype=torch.float32, device=dev)
     lib = L.lib()

@@ -374,8 +374,20 @@ def assoc_case():
     return out
 
 
+def bilinear_case():
+    """The reference's own bilinear_sample (features.py:184-219) on random
+    grids at random, integer, edge and out-of-grid cell coordinates
+    (helpers.bilinear_inputs regenerates the inputs from the seed)."""
+    grids, coords = helpers.bilinear_inputs(np.random.default_rng(71))
+    out = {}
+    for k, (grid, (us, vs)) in enumerate(zip(grids, coords)):
+        pyr = F.FeaturePyramid(0, [F.FeatureGrid(stride=4.0, values=grid)])
+        out[f"out{k}"] = np.stack([F.bilinear_sample(pyr, 0, float(u), float(v)) for u, v in zip(us, vs)])
+    return out
+
+
 def main():
-    jobs = [("paint", paint_case), ("assoc", assoc_case), ("visibility", visibility_case), ("fpyr", fpyr_case), ("crit1", crit1), ("features", features_cases), ("bench", bench_cases), ("dense", dense_cases),
+    jobs = [("bilinear", bilinear_case), ("paint", paint_case), ("assoc", assoc_case), ("visibility", visibility_case), ("fpyr", fpyr_case), ("crit1", crit1), ("features", features_cases), ("bench", bench_cases), ("dense", dense_cases),
             ("projection", projection_cases), ("oae", oae_cases)]
     only = set(sys.argv[1:])
     for name, fn in jobs:

@@ -83,6 +83,25 @@ def make_dense(rng, bs=1, n_q=5, n_p=3, cams=2, n_levels=2, groups=2, channels=8
     return grids, shape, loc, wts
 
 
+def bilinear_inputs(rng, n_grids=4, n_coords=200):
+    """Grids and (u, v) cell coordinates for bilinear_sample fixtures: random
+    coordinates over [-2, W+1] x [-2, H+1], exact integers (cell centres),
+    the last row/column, halves, and values just outside the grid."""
+    grids, coords = [], []
+    for k in range(n_grids):
+        h, w, c = int(rng.integers(2, 12)), int(rng.integers(2, 12)), 2 * int(rng.integers(1, 40))
+        grid = rng.standard_normal((h, w, c)).astype(np.float32)
+        if k == 0:
+            grid[0, 0] = -0.0  # signed zeros in the grid
+        us = rng.uniform(-2.0, w + 1.0, n_coords).astype(np.float32)
+        vs = rng.uniform(-2.0, h + 1.0, n_coords).astype(np.float32)
+        special_u = np.array([0, w - 1, w - 1, -1, -0.5, w - 0.5, 0.5, -1e-7, w - 1 + 1e-6, 3.0], np.float32)
+        special_v = np.array([0, h - 1, 0, -1, -0.5, h - 0.5, 0.5, -1e-7, h - 1 + 1e-6, -0.0], np.float32)
+        grids.append(grid)
+        coords.append((np.concatenate([us, special_u]), np.concatenate([vs, special_v])))
+    return grids, coords
+
+
 def per_query_hash(per_query) -> str:
     import hashlib
 

@@ -146,3 +146,34 @@ def test_bench_reference_arm_contract():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["cpu_baseline"]["value"] == d["value"] and d["cpu_baseline"]["cores"] >= 1
     assert d["config"]["workload"] == "default"
+
+
+def test_sample_plan_from_csr_validates_offsets():
+    """SamplePlan.from_csr enforces the CSR invariant the reference's
+    constructors establish (features.py:122-171): offsets start at 0, never
+    decrease, and end at the per-sample array length."""
+    from paper_2601_10819_b200 import features as F
+
+    one = [1.0] * 3
+    F.SamplePlan.from_csr([0, 1, 3], [0] * 3, [0] * 3, one, one, one)
+    for offs in ([1, 2, 3], [0, 2, 1, 3], [0, 1, 4]):
+        with pytest.raises(ValueError):
+            F.SamplePlan.from_csr(offs, [0] * 3, [0] * 3, one, one, one)
+    with pytest.raises(ValueError):
+        F.SamplePlan.from_csr([0, 3], [0] * 3, [0] * 3, one, one, [1.0, 1.0])
+
+
+def test_bilinear_oracle_matches_reference_golden(golden):
+    """The numpy restatement of bilinear_sample equals the reference's bytes."""
+    import sys
+
+    sys.path.insert(0, str(ROOT / "tests"))
+    import helpers
+    from oracle import msda_oracle as mo
+
+    g = golden("bilinear")
+    grids, coords = helpers.bilinear_inputs(np.random.default_rng(71))
+    for k, (grid, (us, vs)) in enumerate(zip(grids, coords)):
+        h, w, c = grid.shape
+        got = np.stack([mo.bilinear_f32(grid.reshape(h * w, c), (0, h, w), u, v) for u, v in zip(us, vs)])
+        assert got.tobytes() == g[f"out{k}"].tobytes(), k
