@@ -13,8 +13,20 @@ features (270x480 .. 33x60, the reference bench generator's floor halving),
 
 Multi-GPU (torchrun): stream-sharded — every rank owns an independent scene
 (no data-path collective); ``value`` = all ranks' camera-frames / max-rank
-time.  ``--impl reference`` times the reference's CPU algorithm (the oracle
-port of ``msda_optimized``, all host threads) on rank 0 only.
+time.  ``--gpus N`` without torchrun re-launches itself under
+``torch.distributed.run`` with N ranks (one per GPU; it refuses to fold ranks
+onto fewer GPUs unless ``BENCH_SHARE_GPU=1``, a smoke-test mode that is never
+a measurement).  ``--impl reference`` times the reference's own CPU
+implementation (``mvtrack3d.features.msda_optimized`` FULL from
+``baseline/_ref``, all host threads; the oracle port when that install is
+absent) on rank 0 only.
+
+At N = 1 the line also carries a ``sparse4d`` block: the north_star operator
+``deformable_aggregation`` at cfg1 (f32, f16), cfg2 (dense), cfg4 (bf16) and
+the paper headline cfg3 (64 fp16 cameras, one frame = 6 decoder layers in one
+CUDA graph), each checked against the C oracle before it is timed (EXACT:
+bytes; FAST: 1e-4; FAST_H2: 1e-2), timed cold (L2 flushed) and warm with
+CUDA events inside its own clock-sampling window.
 """
 
 from __future__ import annotations
@@ -185,21 +197,85 @@ def l2_gather_ceiling():
     return best
 
 
-def cpu_reference_time(gw, budget_s=15.0, reps=3, workers=None):
-    """Time the reference CPU algorithm (oracle port of msda_optimized FULL,
-    all host threads) on a bounded query sample; returns per-full-call seconds."""
+def reference_features():
+    """The UNMODIFIED reference's ``mvtrack3d.features`` from ``baseline/_ref``
+    (pip install of /root/reference), or None when absent."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "mvtrack3d" / "features.py").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        from mvtrack3d import features as rf
+    except Exception as e:  # pragma: no cover - broken install
+        log(f"baseline/_ref present but mvtrack3d does not import ({e}); timing the oracle port")
+        return None
+    return rf
+
+
+def host_metadata():
+    """The reference's _host_metadata() (bench.py:130-139) plus the CPU model (lscpu)."""
+    import platform
+
+    md = {"platform": platform.platform(), "machine": platform.machine(), "python": platform.python_version(),
+          "numpy": np.__version__, "cpu_count": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    md["cpu_model"] = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        md["affinity_cores"] = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        pass
+    return md
+
+
+def _cpu_impl(gw, workers):
+    """A callable running the reference CPU algorithm on the first nq queries
+    of the workload: the real mvtrack3d msda_optimized(FULL) when installed
+    (kind "reference"), else the oracle port msda_tiled (kind "port")."""
+    wl = gw.workload
+    rf = reference_features()
+    if rf is not None:
+        pyrs = []
+        for c in range(wl.cameras):
+            lv = []
+            for m, (h, w) in enumerate(wl.level_dims()):
+                st = int(gw.tile_start[c * wl.levels + m])
+                lv.append(rf.FeatureGrid(stride=wl.strides()[m], values=gw.table[st:st + h * w].reshape(h, w, -1)))
+            pyrs.append(rf.FeaturePyramid(c, lv))
+
+        def run(nq):
+            s = int(gw.offsets[nq])
+            plan = rf.SamplePlan.__new__(rf.SamplePlan)
+            plan._finalize(np.ascontiguousarray(gw.offsets[:nq + 1]), gw.camera_ids[:s], gw.levels[:s], gw.us[:s],
+                           gw.vs[:s], gw.weights[:s])
+            return rf.msda_optimized(pyrs, plan, rf.PrecisionMode.FULL, workers=workers)
+        return run, "reference", "mvtrack3d.features.msda_optimized(FULL, workers=%d) from baseline/_ref" % workers
     from oracle import msda_oracle as mo
 
+    def run(nq):
+        s = int(gw.offsets[nq])
+        return mo.msda_tiled(gw.table, gw.tiles, wl.levels, gw.offsets[:nq + 1], gw.camera_ids[:s], gw.levels[:s],
+                             gw.us[:s], gw.vs[:s], gw.weights[:s], precision="full", workers=workers)
+    return run, "port", "oracle.msda_oracle.msda_tiled (msda_optimized FULL restated, numpy, ThreadPool)"
+
+
+def cpu_reference_time(gw, budget_s=15.0, reps=3, workers=None):
+    """Time the reference CPU algorithm (all host threads) on a bounded query
+    sample; returns per-full-call seconds."""
     workers = workers or os.cpu_count() or 1
     wl = gw.workload
     per_q = wl.cameras * wl.levels * wl.points_per_query
+    impl, kind, algo = _cpu_impl(gw, workers)
 
     def run(nq):
-        offs = gw.offsets[:nq + 1]
-        s = int(offs[-1])
         t0 = time.perf_counter()
-        out, _ = mo.msda_tiled(gw.table, gw.tiles, wl.levels, offs, gw.camera_ids[:s], gw.levels[:s], gw.us[:s],
-                               gw.vs[:s], gw.weights[:s], precision="full", workers=workers)
+        out, _ = impl(nq)
         return time.perf_counter() - t0, out
 
     # The tile-grouped algorithm has a per-(camera, level) cost that a query
@@ -215,7 +291,13 @@ def cpu_reference_time(gw, budget_s=15.0, reps=3, workers=None):
         times.append(t)
     mean = float(np.mean(times))
     return {"full_call_s": mean * wl.queries / nq, "sample_queries": nq, "per_q_samples": per_q,
-            "workers": workers, "times_s": times, "out": out}
+            "workers": workers, "times_s": times, "out": out, "kind": kind, "algorithm": algo}
+
+
+def csr_config(args, cfg, wl):
+    """The ``config`` object both arms print (identical keys and values)."""
+    return {"workload": args.config, "desc": cfg["desc"],
+            **{k: (list(v) if isinstance(v, tuple) else v) for k, v in wl.to_dict().items()}}
 
 
 def run_reference(args, cfg, rank, world):
@@ -228,18 +310,13 @@ def run_reference(args, cfg, rank, world):
     r = cpu_reference_time(gw, budget_s=max(1.0, 180.0 / max(1, args.steps + args.warmup)), reps=1,
                            workers=workers)
     nq = r["sample_queries"]
-    from oracle import msda_oracle as mo
-
-    s = int(gw.offsets[nq])
-    step = lambda: mo.msda_tiled(gw.table, gw.tiles, wl.levels, gw.offsets[:nq + 1], gw.camera_ids[:s],  # noqa
-                                 gw.levels[:s], gw.us[:s], gw.vs[:s], gw.weights[:s], precision="full",
-                                 workers=workers)
+    impl, kind, algo = _cpu_impl(gw, workers)
     for _ in range(args.warmup):
-        step()
+        impl(nq)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        step()
+        impl(nq)
         times.append(time.perf_counter() - t0)
     t_full = float(np.mean(times)) * wl.queries / nq
     value = wl.cameras / t_full
@@ -250,11 +327,9 @@ def run_reference(args, cfg, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "camera-frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference generate_workload)",
-        "config": {"workload": args.config, "desc": cfg["desc"], **{k: (list(v) if isinstance(v, tuple) else v)
-                                                                     for k, v in wl.to_dict().items()}},
-        "cpu_baseline": {"value": value, "unit": "camera-frames/s", "cores": workers, "kind": "port",
-                         "sample": sample, "algorithm": "oracle.msda_oracle.msda_tiled (msda_optimized FULL "
-                                                        "restated, numpy, ThreadPool over queries)"},
+        "config": csr_config(args, cfg, wl),
+        "cpu_baseline": {"value": value, "unit": "camera-frames/s", "cores": workers, "kind": kind,
+                         "sample": sample, "algorithm": algo, "host": host_metadata()},
         "e2e": {"value": value, "unit": "camera-frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -267,6 +342,9 @@ def rank_device(local_rank):
 
     if os.environ.get("BENCH_SHARE_GPU") == "1":
         return torch.device("cuda", local_rank % torch.cuda.device_count()), "gloo"
+    if local_rank >= torch.cuda.device_count():
+        raise SystemExit(f"rank {local_rank}: only {torch.cuda.device_count()} visible GPU(s); one rank per GPU "
+                         "(BENCH_SHARE_GPU=1 folds ranks for a smoke test, never for a measurement)")
     return torch.device("cuda", local_rank), "nccl"
 
 
@@ -438,11 +516,11 @@ def run_ours(args, cfg, rank, local_rank, world):
         "metric": METRIC, "value": value, "unit": "camera-frames/s", "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (reference generate_workload bytes, seed=rank)",
-        "config": {"workload": args.config, "desc": cfg["desc"], "precision": "exact (bit-identical)",
-                   "parallelism": f"stream-sharded x{world} (independent scenes, no collective)",
-                   "l2": ("flushed between steps (2x L2 write)" if flush else
-                          f"inputs larger than L2 ({table_bytes / 1e9:.2f} GB table), no flush"),
-                   **{k: (list(v) if isinstance(v, tuple) else v) for k, v in wl.to_dict().items()}},
+        "config": csr_config(args, cfg, wl),
+        "precision": "exact (bit-identical)",
+        "parallelism": f"stream-sharded x{world} (independent scenes, no collective)",
+        "l2": ("flushed between steps (2x L2 write)" if flush else
+               f"inputs larger than L2 ({table_bytes / 1e9:.2f} GB table), no flush"),
         "latency_us": ms_per_step * 1e3,
         "stage_us": {"plan_canon": float(np.mean(plan_ms)) * 1e3, "gather_exact": g_ms * 1e3,
                      "note": "stages timed apart (events between them); the step is one call"},
@@ -489,21 +567,173 @@ def run_ours(args, cfg, rank, local_rank, world):
         parity = r["out"].tobytes() == out.cpu().numpy()[:nq].tobytes()
         line["cpu_baseline"] = {
             "value": wl.cameras / r["full_call_s"], "unit": "camera-frames/s", "cores": r["workers"],
-            "kind": "port",
+            "kind": r["kind"],
             "sample": (f"full workload ({wl.num_samples} samples) x3 reps after 1 warm-up" if nq == wl.queries
                        else f"{nq} of {wl.queries} queries x3 reps (1 warm-up), extrapolated linearly"),
-            "algorithm": "oracle msda_tiled (reference msda_optimized FULL restated, numpy, threads)",
+            "algorithm": r["algorithm"], "host": host_metadata(),
             "gpu_bitwise_equal_on_sample": bool(parity)}
         # SURVEY §8(d) also asks for the single-thread figure (msda_optimized, workers=1): one bounded rep
         r1 = cpu_reference_time(gw, budget_s=12.0, reps=1, workers=1)
         line["cpu_baseline"]["single_thread"] = {
-            "value": wl.cameras / r1["full_call_s"], "unit": "camera-frames/s", "cores": 1,
+            "value": wl.cameras / r1["full_call_s"], "unit": "camera-frames/s", "cores": 1, "kind": r1["kind"],
             "sample": (f"full workload x1 rep after 1 warm-up" if r1["sample_queries"] == wl.queries
                        else f"{r1['sample_queries']} of {wl.queries} queries x1 rep, extrapolated linearly")}
+    if world == 1 and not args.no_sparse4d:
+        del feats, plan_d, host_table, gw, pyrs, plan_h
+        torch.cuda.empty_cache()
+        line["sparse4d"] = sparse4d_block(args, dev, smi_index)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+SPARSE4D_CASES = [
+    # (key, BASELINE config, cams, levels, dtype, precisions timed; the first is the case's headline)
+    ("cfg1_f32", "configs[0] Sparse4D default: 6 cams, 64x176..8x22, 900 anchors, 13 pts, C=256, G=8, fp32", 6,
+     "CFG1_LEVELS", "float32", ["fast", "exact"]),
+    ("cfg1_f16", "configs[0] shape, fp16 features (PAPER.md's H100 fp16 comparison)", 6, "CFG1_LEVELS", "float16",
+     ["fast_h2", "fast"]),
+    ("cfg2_dense_f32", "configs[1] shape as the Sparse4D dense operator: 16 cams, 1080p levels 270x480..34x60, fp32",
+     16, "CFG2_LEVELS", "float32", ["fast"]),
+    ("cfg4_bf16", "configs[3] MSDA part: 32 cams at the cfg1 shape, bf16", 32, "CFG1_LEVELS", "bfloat16",
+     ["fast", "exact"]),
+    ("cfg3_f16", "configs[2] paper headline, one decoder layer: 64 cams at the cfg1 shape, fp16", 64, "CFG1_LEVELS",
+     "float16", ["fast_h2", "fast", "exact"]),
+]
+
+
+def _time_events(fn, reps, stream, flush_buf=None):
+    """Per-call CUDA-event times (ms) on ``stream``; ``flush_buf`` (> L2) is
+    rewritten before every call (cold) or not at all (warm, back to back)."""
+    import torch
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    torch.cuda.synchronize()
+    for a, b in ev:
+        if flush_buf is not None:
+            flush_buf.zero_()
+        a.record(stream)
+        fn()
+        b.record(stream)
+    torch.cuda.synchronize()
+    return sorted(a.elapsed_time(b) for a, b in ev)
+
+
+def sparse4d_block(args, dev, smi_index):
+    """deformable_aggregation (north_star's operator) at the BASELINE shapes,
+    under this run's clock: oracle parity first, then cold / warm timing."""
+    import torch
+
+    from oracle import build as ob  # the parity checker (test infrastructure), never the thing timed
+    from paper_2601_10819_b200 import ops
+    from tools import sparse4d_cases as s4
+
+    peak, peak_src = measured_peak_hbm()
+    ceiling = l2_gather_ceiling()
+    stream = torch.cuda.current_stream(dev)
+    flush_buf = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev)
+    reps = max(5, args.steps)
+    Q, P, G, C, L = 900, 13, 8, 256, 4
+    res = {"note": "deformable_aggregation(mc_ms_feat, spatial_shape, scale_start_index, sampling_location, weights),"
+                   " normalize=False (softmaxed weights, as Sparse4D); synthetic inputs per SURVEY 8(d); every "
+                   "case is checked against the C oracle (oracle/msda_oracle.c, pinned to the reference) on the "
+                   "features the GPU reads before it is timed; cold = L2 flushed (2x L2 write) before every call, "
+                   "warm = back-to-back calls (the decoder-layer situation: same table, new anchors)",
+           "peak_gbs": peak, "peak_source": peak_src, "l2_gather_ceiling_gbs": ceiling, "reps": reps, "cases": {}}
+    clocks = ClockSampler(smi_index)
+    clocks.start()
+    time.sleep(0.2)
+    t_block = time.time()
+    for key, desc, cams, lv_name, dt_name, precs in SPARSE4D_CASES:
+        levels = getattr(s4, lv_name)
+        dtype = getattr(torch, dt_name)
+        esize = torch.finfo(dtype).bits // 8
+        feats = s4.make_feats(cams, levels, C, dtype, dev, seed=cams)
+        loc, w = s4.make_dense_inputs(1, Q, P, cams, L, G, dev, seed=100 + cams)
+        out = torch.empty((1, Q, C), dtype=torch.float32, device=dev)
+        ab = s4.algorithmic_bytes(feats, loc, w, esize)
+        # ---- parity against the C oracle on the features the GPU reads ----
+        t0 = time.time()
+        table, tiles, shape = s4.host_view(feats)
+        ref = ob.msda_dense_groups_c(table, tiles, shape, loc.cpu().numpy(), w.cpu().numpy(), L, normalize=False)
+        del table
+        oracle_s = time.time() - t0
+        scale = float(np.abs(ref).max())
+        case = {"desc": desc, "cams": cams, "dtype": dt_name, "queries": Q, "points": P, "groups": G, "channels": C,
+                "levels": [list(x) for x in levels], "algorithmic_bytes": ab,
+                "l2": "flushed per call" if feats.table.numel() * esize < 2 * L2_BYTES else "table larger than L2",
+                "oracle_s": oracle_s, "paths": {}}
+        for prec in precs:
+            fn = (lambda p=prec: ops.deformable_aggregation(feats, None, None, loc, w, precision=p, out=out))  # noqa
+            ops.deformable_aggregation(feats, None, None, loc, w, precision=prec, out=out, check=True)
+            got = out.cpu().numpy()
+            err = float(np.abs(got - ref).max() / max(1e-12, scale))
+            if prec == "exact":
+                ok = got.tobytes() == ref.tobytes()
+                parity = {"bitwise_equal_to_oracle": bool(ok)}
+            else:
+                tol = 1e-2 if prec == "fast_h2" else 1e-4
+                ok = float(np.abs(got - ref).max() / (max(1.0, scale) if prec == "fast_h2" else scale)) <= tol
+                parity = {"max_rel_err_vs_oracle": err, "tolerance": tol, "within_tolerance": bool(ok)}
+            for _ in range(3):
+                fn()
+            cold = _time_events(fn, reps, stream, flush_buf)
+            warm = _time_events(fn, reps, stream)
+            med_c, med_w = cold[len(cold) // 2], warm[len(warm) // 2]
+            achieved = ab["total"] / (med_c / 1e3) / 1e9
+            case["paths"][prec] = {
+                **parity, "latency_us": med_c * 1e3, "best_us": cold[0] * 1e3, "warm_us": med_w * 1e3,
+                "camera_frames_per_s": cams / (med_c / 1e3),
+                "streams_at_30fps_6layers": int(cams / (30 * 6 * med_c / 1e3)),
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak},
+                "l2_gather": {"bytes": ab["gathered_corner_bytes"],
+                              "achieved_gbs": ab["gathered_corner_bytes"] / (med_c / 1e3) / 1e9,
+                              "frac_of_ceiling": (ab["gathered_corner_bytes"] / (med_c / 1e3) / 1e9 / ceiling)
+                              if ceiling else None}}
+        if key == "cfg3_f16":
+            case["frame"] = _cfg3_frame(feats, dev, stream, reps, Q, P, G, C, L, cams)
+        res["cases"][key] = case
+        del feats, loc, w, out, ref
+        torch.cuda.empty_cache()
+    res["block_s"] = time.time() - t_block
+    res["clocks"] = clocks.stop()
+    return res
+
+
+def _cfg3_frame(feats, dev, stream, reps, Q, P, G, C, L, cams, layers=6):
+    """The paper headline (BASELINE configs[2]): one frame of 64 fp16 camera
+    streams = 6 decoder layers of deformable_aggregation, each with its own
+    sampling locations and weights, captured once in a CUDA graph and
+    replayed back to back (no host work between layers)."""
+    import torch
+
+    from paper_2601_10819_b200 import ops
+    from tools import sparse4d_cases as s4
+
+    ins = [s4.make_dense_inputs(1, Q, P, cams, L, G, dev, seed=200 + k) for k in range(layers)]
+    outs = [torch.empty((1, Q, C), dtype=torch.float32, device=dev) for _ in range(layers)]
+    frame = {}
+    for prec in ("fast_h2", "fast"):
+        def run(p=prec):
+            for (loc, w), o in zip(ins, outs):
+                ops.deformable_aggregation(feats, None, None, loc, w, precision=p, out=o)
+        run()  # workspace allocation outside the capture
+        torch.cuda.synchronize()
+        cap = torch.cuda.Stream(dev)
+        cap.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cap):
+            run()
+        graph.replay()
+        torch.cuda.synchronize()
+        t = _time_events(graph.replay, reps, stream)
+        med = t[len(t) // 2]
+        frame[prec] = {"frame_us": med * 1e3, "per_layer_us": med * 1e3 / layers, "frames_per_s": 1e3 / med,
+                       "camera_streams_at_30fps": int(cams * (1e3 / med) / 30), "layers": layers}
+        del graph
+    return frame
 
 
 DENSE_CONFIGS = {
@@ -607,6 +837,64 @@ def run_dense_scaling(args, cfg, rank, local_rank, world):
         dist.destroy_process_group()
 
 
+def launch_ranks(args):
+    """``--gpus N`` without torchrun: re-run this script under
+    ``torch.distributed.run`` with N ranks on this node (127.0.0.1), one per
+    GPU.  Refuses (exit 2) when fewer than N GPUs are visible, unless
+    BENCH_SHARE_GPU=1 (ranks folded onto the visible GPUs over gloo: a smoke
+    test of the multi-rank path, never a measurement)."""
+    import socket
+
+    if os.environ.get("BENCH_PLUMBING") != "1":
+        import torch
+
+        n = torch.cuda.device_count()
+        if n < args.gpus and os.environ.get("BENCH_SHARE_GPU") != "1":
+            log(f"bench.py --gpus {args.gpus}: only {n} GPU(s) visible; one rank per GPU is required "
+                "(BENCH_SHARE_GPU=1 folds ranks for a smoke test, not a measurement)")
+            return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    log("launching: " + " ".join(cmd))
+    return subprocess.call(cmd)
+
+
+def run_plumbing(args, rank, world):
+    """BENCH_PLUMBING=1 (CPU tests only): the multi-rank launch, barrier,
+    max-over-ranks and JSON path of the bench over gloo with a trivial host
+    step — no GPU, no measurement."""
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    import torch
+
+    a = np.ones((256, 256), dtype=np.float32)
+    for _ in range(args.warmup):
+        a @ a
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        a @ a
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": "camera-frames/s", "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(t.item()) / args.steps * 1e3,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                          "data": "plumbing test (BENCH_PLUMBING=1): no GPU, no measurement",
+                          "config": {"workload": args.config}}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -616,9 +904,17 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-sparse4d", action="store_true", help="skip the sparse4d block")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     rank, local_rank, world = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        sys.exit(launch_ranks(args))
+    if args.impl == "ours" and world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
+    if os.environ.get("BENCH_PLUMBING") == "1":
+        run_plumbing(args, rank, world)
+        return
     if args.config in DENSE_CONFIGS:
         run_dense_scaling(args, DENSE_CONFIGS[args.config], rank, local_rank, world)
         return

@@ -79,3 +79,23 @@ def msda_c(table, tiles, n_levels, offsets, cam, lvl, u, v, w, normalize=True, h
     if st != 0:
         raise RuntimeError(f"oracle status {st}")
     return out, empty.astype(bool)
+
+
+def msda_dense_groups_c(table, tiles, spatial_shape, sampling_location, weights, n_levels, normalize=False,
+                        threads=0):
+    """Dense Sparse4D layout with channel groups through the C oracle (full
+    BASELINE sizes): group g's channel slice = msda_reference over the
+    group's CSR plan (SURVEY §8(c) "Groups G"), bs = 1.  ``table`` is the
+    f32 view of the features the GPU reads (f16/bf16 widened exactly)."""
+    from . import msda_oracle as mo
+
+    g_n = weights.shape[-1]
+    c_n = table.shape[1]
+    cpg = c_n // g_n
+    bs, q_n = sampling_location.shape[:2]
+    out = np.empty((bs * q_n, c_n), dtype=np.float32)
+    for g in range(g_n):
+        plan = mo.dense_to_csr_vectorized(spatial_shape, sampling_location, weights, g)
+        sub = np.ascontiguousarray(table[:, g * cpg:(g + 1) * cpg], dtype=np.float32)
+        out[:, g * cpg:(g + 1) * cpg], _ = msda_c(sub, tiles, n_levels, *plan, normalize=normalize, threads=threads)
+    return out.reshape(bs, q_n, c_n)

@@ -280,6 +280,24 @@ def dense_to_csr(spatial_shape, sampling_location, weights, group, n_levels):
     return offsets, pick(1, np.int32), pick(2, np.int32), pick(3, np.float32), pick(4, np.float32), pick(5, np.float32)
 
 
+def dense_to_csr_vectorized(spatial_shape, sampling_location, weights, group):
+    """``dense_to_csr`` vectorised (full BASELINE sizes): the same samples in
+    the same per-query order (point, camera, level) with the same f32 cell
+    arithmetic ``f32(f32(x * W_l) - 0.5)`` (features.py:20-24, 45-47)."""
+    bs, q_n, p_n, cams, _ = sampling_location.shape
+    n_levels = spatial_shape.shape[1]
+    W = spatial_shape[:, :, 1].astype(F32)[None, None, None]  # [1, 1, 1, cams, L]
+    H = spatial_shape[:, :, 0].astype(F32)[None, None, None]
+    u = (sampling_location[..., 0:1].astype(F32) * W).astype(F32) - F32(0.5)
+    v = (sampling_location[..., 1:2].astype(F32) * H).astype(F32) - F32(0.5)
+    cam = np.broadcast_to(np.arange(cams, dtype=np.int32)[None, None, None, :, None], u.shape)
+    lvl = np.broadcast_to(np.arange(n_levels, dtype=np.int32)[None, None, None, None, :], u.shape)
+    per_q = p_n * cams * n_levels
+    offsets = np.arange(bs * q_n + 1, dtype=np.int64) * per_q
+    return (offsets, cam.reshape(-1).copy(), lvl.reshape(-1).copy(), u.astype(F32).reshape(-1),
+            v.astype(F32).reshape(-1), np.ascontiguousarray(weights[..., group], dtype=F32).reshape(-1))
+
+
 def msda_dense_groups(table, tiles, spatial_shape, sampling_location, weights, n_levels, normalize=False):
     """Group oracle: group g's channel slice aggregated with weights[..., g].
 

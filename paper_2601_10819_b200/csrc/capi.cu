@@ -120,15 +120,6 @@ int num_sms_for_current_device() {
   return n;
 }
 
-// MSDA_HOST_FETCH=0 copies every grid of the host-buffer path whole
-bool fetch_enabled() {
-  static const bool v = [] {
-    const char* e = getenv("MSDA_HOST_FETCH");
-    return !(e && e[0] == '0');
-  }();
-  return v;
-}
-
 int32_t validate_features(const msda_features_t* f) {
   if (!f || !f->data || !f->spatial_shape || !f->scale_start_index) return MSDA_BAD_ARG;
   if (f->n_cams <= 0 || f->n_levels <= 0 || f->channels <= 0 || f->batch <= 0) return MSDA_BAD_ARG;
@@ -339,10 +330,10 @@ int32_t msda_csr_host(msda_context_t* ctx, const void* const* level_data, const 
   // tiles fetched row by row instead of copied whole: pinned (device-visible)
   // host buffers of grids with more cells than 2 x the mean samples per tile
   // (4 corner reads per sample touch < ~85 % of such a grid; measured at cfg2:
-  // fetching levels 0-1 beats copying them, MSDA_HOST_FETCH=0: copy all)
+  // fetching levels 0-1 beats copying them)
   std::vector<unsigned long long> src(n_tiles, 0ull);
   const int64_t per_tile = n_tiles > 0 ? S / n_tiles : 0;
-  const bool fetch_ok = !cvt_half && fetch_enabled() && (channels * esz) % 16 == 0;
+  const bool fetch_ok = !cvt_half && (channels * esz) % 16 == 0;
   for (int t = 0; t < n_tiles && fetch_ok; ++t) {
     const int64_t cells = (int64_t)spatial_shape[2 * t] * spatial_shape[2 * t + 1];
     if (cells <= 2 * per_tile || !level_data[t]) continue;

@@ -610,15 +610,6 @@ size_t dense_exact_extra_bytes(int64_t n_queries, int64_t n_samples) {
   return align_up((size_t)(n_queries + 1) * 8, 256) + 5 * align_up((size_t)n_samples * 4, 256);
 }
 
-// MSDA_DENSE_PIPE=0 keeps dense FAST on the warp-camera kernel (A/B runs)
-bool dense_pipe_enabled() {
-  static const bool v = [] {
-    const char* e = getenv("MSDA_DENSE_PIPE");
-    return !(e && e[0] == '0');
-  }();
-  return v;
-}
-
 int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, const float* loc, const float* w,
                   int32_t precision, int32_t normalize, float* out, void* ws, size_t ws_bytes, cudaStream_t s,
                   bool project, const float* anchors, int32_t n_learned, const float* offsets,
@@ -695,7 +686,7 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
   if (nq == 0) return MSDA_OK;
   if (precision == MSDA_FAST || precision == MSDA_FAST_H2) {
     const bool h2 = precision == MSDA_FAST_H2;
-    if (!project && dense_pipe_enabled()) {  // pipelined gather (msda_exact.cu), else the warp-camera kernel
+    if (!project) {  // pipelined gather (msda_exact.cu); shapes it does not take use the warp-camera kernel
       // the exact records' space is free in FAST: it holds the split weight sums
       float* scratch = reinterpret_cast<float*>(ew.rec);
       const DenseFastSpec d{loc, w, Q, P, G, normalize, wsum_out, scratch, h2};

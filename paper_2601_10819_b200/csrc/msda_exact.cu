@@ -912,14 +912,6 @@ cudaError_t launch_gather(const GatherArgs& g, cudaStream_t stream, bool raw) {
   return cudaGetLastError();
 }
 
-int f32_lane_bytes() {
-  static const int v = [] {
-    const char* e = getenv("MSDA_F32_LANE_BYTES");
-    return (e && atoi(e) == 8) ? 8 : 16;
-  }();
-  return v;
-}
-
 }  // namespace
 
 cudaError_t launch_gather_dense_fast(const msda_features_t& f, const DenseFastSpec& d, DevStatus* status, float* out,
@@ -1100,8 +1092,7 @@ cudaError_t launch_gather_exact(const msda_features_t& f, const msda_csr_plan_t&
   }
   switch (f.dtype) {
     case MSDA_F32:
-      // two warps per 256 channels (16-B lanes) or, with MSDA_F32_LANE_BYTES=8, four (8-B lanes)
-      if (f32_lane_bytes() == 8 && C % 64 == 0 && base % 8 == 0) return launch_gather<float, 2, false>(g, stream, raw);
+      // two warps per 256 channels (16-B lanes; 8-B lanes measured slower)
       if (C % 4 == 0 && base % 16 == 0 && obase % 16 == 0) return launch_gather<float, 4, false>(g, stream, raw);
       return launch_gather<float, 2, false>(g, stream, raw);
     case MSDA_F16:

@@ -405,7 +405,9 @@ def msda_optimized(pyramids, plan: SamplePlan, precision: PrecisionMode = Precis
     channels = next(iter(pyr_map.values())).channels if pyr_map else 0
     if channels % 2 != 0:
         raise OddChannelCount(f"channel count {channels} is odd; packed pairs need an even count")
-    if not isinstance(precision, PrecisionMode):
+    # this module's PrecisionMode or the reference's own enum (same values)
+    if not (isinstance(precision, Enum) and type(precision).__name__ == "PrecisionMode"
+            and precision.value in ("full", "half")):
         raise ValueError(f"unknown precision mode: {precision!r}")
-    code = L.MSDA_EXACT if precision is PrecisionMode.FULL else L.MSDA_EXACT_HALF
+    code = L.MSDA_EXACT if precision.value == "full" else L.MSDA_EXACT_HALF
     return _run(pyramids, plan, code, normalize, device)

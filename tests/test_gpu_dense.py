@@ -362,24 +362,6 @@ def test_camera_sharded_partials_on_device(cuda_dev):
         agg(t(loc), t(zero), normalize=True)
 
 
-def _dense_csr_vectorized(shape, loc, wts, group):
-    """dense_to_csr (oracle/msda_oracle.py) vectorised: same samples, same
-    per-query order (point, camera, level), same f32 cell arithmetic."""
-    bs, q_n, p_n, cams, _ = loc.shape
-    n_levels = shape.shape[1]
-    F32 = np.float32
-    W = shape[:, :, 1].astype(F32)[None, None, None]  # [1, 1, 1, cams, L]
-    H = shape[:, :, 0].astype(F32)[None, None, None]
-    u = (loc[..., 0:1].astype(F32) * W).astype(F32) - F32(0.5)
-    v = (loc[..., 1:2].astype(F32) * H).astype(F32) - F32(0.5)
-    cam = np.broadcast_to(np.arange(cams, dtype=np.int32)[None, None, None, :, None], u.shape)
-    lvl = np.broadcast_to(np.arange(n_levels, dtype=np.int32)[None, None, None, None, :], u.shape)
-    per_q = p_n * cams * n_levels
-    offsets = np.arange(bs * q_n + 1, dtype=np.int64) * per_q
-    return (offsets, cam.reshape(-1).copy(), lvl.reshape(-1).copy(), u.astype(F32).reshape(-1),
-            v.astype(F32).reshape(-1), wts[..., group].astype(F32).reshape(-1))
-
-
 @pytest.mark.parametrize("dt", ["float32", "float16"])
 def test_dense_exact_full_size_cfg1(c_oracle, cuda_dev, dt):
     """BASELINE configs[0] at full size (6 cams, 64x176 .. 8x22, 900 anchors,
@@ -403,7 +385,7 @@ def test_dense_exact_full_size_cfg1(c_oracle, cuda_dev, dt):
                                      check=True).cpu().numpy().reshape(Q, C)
     cpg = C // G
     for g in range(G):
-        plan = _dense_csr_vectorized(shape, loc, wts, g)
+        plan = mo.dense_to_csr_vectorized(shape, loc, wts, g)
         ref, _ = c_oracle.msda_c(np.ascontiguousarray(seen[:, g * cpg:(g + 1) * cpg]), tiles, 4, *plan)
         assert out[:, g * cpg:(g + 1) * cpg].tobytes() == ref.tobytes(), g
 

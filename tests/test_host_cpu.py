@@ -146,6 +146,36 @@ def test_bench_reference_arm_contract():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["cpu_baseline"]["value"] == d["value"] and d["cpu_baseline"]["cores"] >= 1
     assert d["config"]["workload"] == "default"
+    # the real reference (baseline/_ref) is timed when installed, else the oracle port
+    assert d["cpu_baseline"]["kind"] == ("reference" if (ROOT / "baseline" / "_ref" / "mvtrack3d").exists()
+                                         else "port")
+    assert "cpu_model" in d["cpu_baseline"]["host"] or d["cpu_baseline"]["host"]["cpu_count"] >= 1
+
+
+def test_bench_launches_n_ranks():
+    """bench.py --gpus 2 without torchrun re-launches itself with 2 ranks
+    (torch.distributed.run, 127.0.0.1): the gloo plumbing mode prints one
+    JSON line with n_gpus = 2; without GPUs and without the fold flag the
+    launcher refuses loudly instead of timing one rank."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--steps", "2", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env={**env, "BENCH_PLUMBING": "1"})
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] is None and "no measurement" in d["data"]
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--steps", "1"],
+                           capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+        assert r.returncode == 2 and "one rank per GPU" in r.stderr
 
 
 def test_sample_plan_from_csr_validates_offsets():

@@ -25,9 +25,8 @@ sys.path.insert(0, str(ROOT))
 
 from paper_2601_10819_b200 import ops  # noqa: E402
 
-CFG1_LEVELS = [(64, 176), (32, 88), (16, 44), (8, 22)]
-CFG2_LEVELS = [(270, 480), (135, 240), (68, 120), (34, 60)]
-L2 = 126 * 1024 * 1024
+from tools.sparse4d_cases import CFG1_LEVELS, CFG2_LEVELS, L2_BYTES as L2, make_dense_inputs  # noqa: E402
+from tools.sparse4d_cases import make_feats as _make_feats, touched_bytes  # noqa: E402
 
 
 def peak():
@@ -36,50 +35,7 @@ def peak():
 
 
 def make_feats(cams, levels, C, dtype, dev, bs=1):
-    rows = cams * sum(h * w for h, w in levels)
-    g = torch.Generator(device=dev).manual_seed(0)
-    table = (torch.rand((bs, rows, C), generator=g, device=dev) * 2 - 1).to(dtype)
-    shape = torch.tensor([[list(l) for l in levels]] * cams, dtype=torch.int32)
-    start, r = [], 0
-    for _ in range(cams):
-        s = []
-        for h, w in levels:
-            s.append(r)
-            r += h * w
-        start.append(s)
-    return ops.DeviceFeatures(table, shape, torch.tensor(start, dtype=torch.int64))
-
-
-def make_dense_inputs(bs, Q, P, cams, L, G, dev):
-    g = torch.Generator(device=dev).manual_seed(1)
-    loc = torch.rand((bs, Q, P, cams, 2), generator=g, device=dev)
-    logits = torch.randn((bs, Q, P * cams * L, G), generator=g, device=dev)
-    w = torch.softmax(logits, dim=2).reshape(bs, Q, P, cams, L, G).contiguous()
-    return loc, w
-
-
-def touched_bytes(feats, loc, esize):
-    """Unique in-bounds corner cells of the dense sampling."""
-    shape = feats.spatial_shape.long()
-    start = feats.scale_start_index
-    bs, Q, P, cams, _ = loc.shape
-    L = shape.shape[1]
-    idx = []
-    for c in range(cams):
-        for m in range(L):
-            H, W = int(shape[c, m, 0]), int(shape[c, m, 1])
-            u = loc[:, :, :, c, 0] * W - 0.5
-            v = loc[:, :, :, c, 1] * H - 0.5
-            x0, y0 = torch.floor(u).long(), torch.floor(v).long()
-            for dy in (0, 1):
-                for dx in (0, 1):
-                    x, y = x0 + dx, y0 + dy
-                    ok = (x >= 0) & (x < W) & (y >= 0) & (y < H)
-                    b = torch.arange(bs, device=loc.device).view(bs, 1, 1).expand_as(x)
-                    idx.append((b * feats.table.shape[1] + int(start[c, m]) + y * W + x)[ok])
-    rows = torch.cat(idx)
-    # (unique touched bytes, bytes of every in-grid corner row the kernel moves L2 -> SM)
-    return torch.unique(rows).numel() * feats.channels * esize, rows.numel() * feats.channels * esize
+    return _make_feats(cams, levels, C, dtype, dev, bs=bs, seed=0)
 
 
 def l2_ceiling():
