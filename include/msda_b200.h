@@ -81,6 +81,9 @@ typedef struct {
   int64_t n_rows;                   /* < 2^31                                        */
   const int32_t *spatial_shape;     /* [n_cams * n_levels * 2] (H, W)                */
   const int64_t *scale_start_index; /* [n_cams * n_levels] first row of each grid    */
+  const int32_t *spatial_shape_host; /* optional HOST copy of spatial_shape, or NULL:
+                                        lets a call pick the on-chip staging plan
+                                        without reading device memory (ABI v2)   */
 } msda_features_t;
 
 /* CSR sample plan (the reference SamplePlan, features.py:112-181).  Camera

@@ -36,7 +36,7 @@ SZ = ctypes.c_size_t
 class Features(ctypes.Structure):
     _fields_ = [("data", P), ("dtype", I32), ("batch", I32), ("n_cams", I32), ("n_levels", I32),
                 ("channels", I32), ("reserved", I32), ("n_rows", I64), ("spatial_shape", P),
-                ("scale_start_index", P)]
+                ("scale_start_index", P), ("spatial_shape_host", P)]
 
 
 class CsrPlan(ctypes.Structure):

@@ -133,7 +133,7 @@ int32_t validate_features(const msda_features_t* f) {
 
 extern "C" {
 
-int32_t msda_abi_version(void) { return 1; }
+int32_t msda_abi_version(void) { return 2; }
 
 const char* msda_status_string(int32_t s) {
   switch (s) {
@@ -444,6 +444,7 @@ int32_t msda_csr_host(msda_context_t* ctx, const void* const* level_data, const 
   f.n_rows = rows;
   f.spatial_shape = d_shape;
   f.scale_start_index = d_start;
+  f.spatial_shape_host = spatial_shape;
   msda_csr_plan_t pl{n_queries, S, d_off, d_cam, d_lvl, d_u, d_v, d_w};
   st = msda_csr(&f, &pl, precision, normalize, d_out, d_emp, d_ws, ws_b, s);
   if (st != MSDA_OK) return fail(st);

@@ -615,6 +615,7 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
                   bool project, const float* anchors, int32_t n_learned, const float* offsets,
                   const msda_cameras_t* cams, const float* strides, float dt, float* wsum_out = nullptr);
 
+
 }  // namespace
 }  // namespace msda
 
@@ -691,7 +692,28 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
       float* scratch = reinterpret_cast<float*>(ew.rec);
       const DenseFastSpec d{loc, w, Q, P, G, normalize, wsum_out, scratch, h2};
       bool pending = false;
-      const cudaError_t e = launch_gather_dense_fast(*f, d, ew.status, out, s, &pending);
+      cudaError_t e = cudaErrorNotSupported;
+      const int n_fine = dense_staged_fine_levels(*f, G, P);
+      if (n_fine > 0) {  // coarse levels from on-chip staged maps, fine levels by the pipelined gather
+        float* wsum = wsum_out ? wsum_out : (normalize ? scratch : nullptr);
+        e = cudaMemsetAsync(out, 0, (size_t)nq * a.C * 4, s);
+        if (e == cudaSuccess && wsum) e = cudaMemsetAsync(wsum, 0, (size_t)nq * G * 4, s);
+        // coarse levels first (issue-bound, no L2 gathers), then the fine
+        // levels' gather; both red.add into the zeroed totals.  (Running them
+        // concurrently on a forked stream measured no better: the fine
+        // gather loses occupancy to the coarse kernel's 121 KB CTAs.)
+        if (e == cudaSuccess) e = launch_dense_coarse(*f, d, n_fine, out, wsum, s);
+        if (e == cudaSuccess) {
+          DenseFastSpec fine = d;
+          fine.n_lv = n_fine;
+          fine.accumulate = true;
+          e = launch_gather_dense_fast(*f, fine, ew.status, out, s, &pending);
+          if (e == cudaErrorNotSupported) return MSDA_CUDA_ERROR;  // the staged plan implies the gather fits
+        }
+        if (e != cudaSuccess) return MSDA_CUDA_ERROR;
+      } else {
+        e = launch_gather_dense_fast(*f, d, ew.status, out, s, &pending);
+      }
       if (e == cudaSuccess) {
         if (pending) {
           const int64_t total = nq * a.C;

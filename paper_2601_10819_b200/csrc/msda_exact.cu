@@ -334,6 +334,8 @@ struct GatherArgs {
   // with n_split > 1 the partial sums are red.add-ed into out / wsum_out
   // (zeroed first) and normalised by a separate pass
   int32_t cps, n_split;
+  int32_t n_lv;        // DENSE: levels [0, n_lv) of every camera
+  int32_t accumulate;  // DENSE: always red.add into the zeroed totals (another kernel adds to them too)
 };
 
 __device__ __forceinline__ SampleRec ld_rec(const SampleRec* p) {
@@ -567,7 +569,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   const int64_t q = gw / warps_per_q;
   if (q >= a.n_queries) return;
   const int c0 = (int)(gw - q * warps_per_q) * 32 * VEC + lane * VEC;
-  const int nd = DENSE ? a.P * n_cam * a.n_levels : 0;  // samples of this dense split
+  const int nd = DENSE ? a.P * n_cam * a.n_lv : 0;  // samples of this dense split
   const int64_t lo = DENSE ? 0 : min(max(a.offsets[q], (int64_t)0), a.n_samples);
   const int n = DENSE ? nd : (int)(min(max(a.offsets[q + 1], lo), a.n_samples) - lo);
   const SampleRec* rec = a.rec + lo;
@@ -606,7 +608,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
     if (s < n) {
       SampleRec r;
       if constexpr (DENSE) {
-        const int per_cam = a.n_levels * a.P;
+        const int per_cam = a.n_lv * a.P;
         const int cs = s / per_cam, rem = s - cs * per_cam;
         const int cam = cam_lo + cs;
         const int l = rem / a.P, p = rem - l * a.P;
@@ -690,7 +692,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   __half2 hacc[HACC ? VEC / 2 : 1];
 #pragma unroll
   for (int e = 0; e < (HACC ? VEC / 2 : 1); ++e) hacc[e] = __float2half2_rn(0.0f);
-  int run_left = HACC ? a.n_levels * a.P : 0;  // samples left in the current camera
+  int run_left = HACC ? a.n_lv * a.P : 0;  // samples left in the current camera
   auto hacc_sample = [&](const RawVec<BYTES>* cv, const float4 iw, const float wn) {
     const float cw[4] = {iw.x * wn, iw.y * wn, iw.z * wn, iw.w * wn};
 #pragma unroll
@@ -708,7 +710,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
         accf[2 * e + 1] += f.y;
         hacc[e] = __float2half2_rn(0.0f);
       }
-      run_left = a.n_levels * a.P;
+      run_left = a.n_lv * a.P;
     }
   };
 
@@ -777,7 +779,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   float* o = a.out + q * a.out_stride + a.c_off + c0;
   if constexpr (DENSE) {  // per-(anchor, group) renormalisation (FAST: sum in any order)
     const bool ghead = (a.c_off + c0) % a.cpg == 0;  // the group's first lane reports
-    if (a.n_split > 1) {  // partial over a camera range: add into the zeroed totals
+    if (a.n_split > 1 || a.accumulate) {  // partial over a camera range: add into the zeroed totals
       if (ghead && a.wsum_out) atomicAdd(a.wsum_out + q * a.n_groups + gl, wsum_g);
       static_assert(VEC % 4 == 0, "float4 partials");
 #pragma unroll
@@ -951,22 +953,41 @@ cudaError_t launch_gather_dense_fast(const msda_features_t& f, const DenseFastSp
   if (C % (32 * vec) || cpg % vec) return cudaErrorNotSupported;
   // cameras per warp: about kDenseSplitSamples samples per warp, so that
   // short per-warp chains and many resident warps keep the gather fed
-  const int per_cam = d.P * f.n_levels;
-  const int want = std::max(1, (f.n_cams * per_cam + kDenseSplitSamples - 1) / kDenseSplitSamples);
+  g.n_lv = d.n_lv > 0 ? std::min(d.n_lv, f.n_levels) : f.n_levels;
+  g.accumulate = d.accumulate ? 1 : 0;
+  const int per_cam = d.P * g.n_lv;
+  const int split_samples = d.accumulate ? kDenseSplitSamples / 2 : kDenseSplitSamples;
+  const int want = std::max(1, (f.n_cams * per_cam + split_samples - 1) / split_samples);
   g.cps = (f.n_cams + want - 1) / want;
   g.n_split = (f.n_cams + g.cps - 1) / g.cps;
-  if (g.n_split > 1) {
+  if (g.n_split > 1 || d.accumulate) {
     if (!d.wsum_out && d.normalize && !d.wsum_scratch) return cudaErrorNotSupported;
     if (!d.wsum_out && d.normalize) g.wsum_out = d.wsum_scratch;
-    if (cudaMemsetAsync(out, 0, (size_t)g.n_queries * C * 4, stream) != cudaSuccess) return cudaErrorUnknown;
-    if (g.wsum_out && cudaMemsetAsync(g.wsum_out, 0, (size_t)g.n_queries * G * 4, stream) != cudaSuccess)
-      return cudaErrorUnknown;
+    if (!d.accumulate) {
+      if (cudaMemsetAsync(out, 0, (size_t)g.n_queries * C * 4, stream) != cudaSuccess) return cudaErrorUnknown;
+      if (g.wsum_out && cudaMemsetAsync(g.wsum_out, 0, (size_t)g.n_queries * G * 4, stream) != cudaSuccess)
+        return cudaErrorUnknown;
+    }
     *normalize_pending = d.normalize != 0;
   }
   // ring depth 2: the dense gather is issue-bound (bf16/f16 -> f32 per
   // channel-corner), so more resident warps (28 per SM at 8 KB of shared
   // memory each) beat a deeper per-warp ring (D = 7: 12 per SM); measured at
   // cfg1-cfg4, D in {2, 3, 4, 5, 7} x split in {104, 156, 208, 416} samples
+  if (d.accumulate) {
+    // fine levels only (the coarse ones come from the staged kernel): every
+    // corner row is an L2 miss or a far L2 hit, so a deeper ring (4 samples
+    // in flight per warp) and shorter chains (104 samples per warp) win —
+    // cfg3 FAST_H2 fine part 227 vs 300 us (D = 2, 208), measured D in
+    // {2, 3, 4, 6, 8} x chains {104, 208, 416}
+    switch (f.dtype) {
+      case MSDA_F16:
+        if (d.h2) return launch_gather_pipe<__half, 8, false, 4, true, 8, true, true>(g, stream);
+        return launch_gather_pipe<__half, 8, false, 4, true, 8, true>(g, stream);
+      case MSDA_BF16: return launch_gather_pipe<__nv_bfloat16, 8, false, 4, true, 8, true>(g, stream);
+      default: return cudaErrorNotSupported;
+    }
+  }
   switch (f.dtype) {
     case MSDA_F32: return launch_gather_pipe<float, 4, false, 2, true, 8, true>(g, stream);
     case MSDA_F16:

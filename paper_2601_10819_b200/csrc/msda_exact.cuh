@@ -43,10 +43,22 @@ struct DenseFastSpec {
   float* wsum_out;      // [batch * Q, G] or null
   float* wsum_scratch;  // [batch * Q, G] device scratch for split normalisation
   bool h2;              // FAST_H2: half2 accumulation per camera (f16 storage; other dtypes ignore it)
+  int32_t n_lv = 0;        // gather only levels [0, n_lv) (0: all)
+  bool accumulate = false;  // out / wsum are zeroed by the caller: always red.add, the caller normalises
 };
 // *normalize_pending: the cameras were split across warps and out holds
 // unnormalised sums; the caller divides by wsum (out or scratch) per group.
 cudaError_t launch_gather_dense_fast(const msda_features_t& f, const DenseFastSpec& d, DevStatus* status, float* out,
                                      cudaStream_t stream, bool* normalize_pending);
+
+// Coarse levels of the dense FAST call from on-chip staged maps
+// (msda_staged.cu).  dense_staged_fine_levels: the number of leading (fine)
+// levels left to the gather when the split applies to this shape (the
+// trailing levels of every camera fit the stage budget), else -1.
+// launch_dense_coarse red.add's the coarse levels' partial sums into the
+// zeroed out / wsum.
+int dense_staged_fine_levels(const msda_features_t& f, int G, int P);
+cudaError_t launch_dense_coarse(const msda_features_t& f, const DenseFastSpec& d, int n_fine, float* out,
+                                float* wsum, cudaStream_t stream);
 
 }  // namespace msda

@@ -119,6 +119,9 @@ class DeviceFeatures:
             raise ValueError("spatial_shape must be [cams, levels, 2]")
         if tuple(self.scale_start_index.shape) != tuple(self.spatial_shape.shape[:2]):
             raise ValueError("scale_start_index must be [cams, levels]")
+        # host copy of the level shapes (C ABI spatial_shape_host): the call
+        # picks its on-chip staging plan without a device read
+        self._shape_host = np.ascontiguousarray(self.spatial_shape.cpu().numpy(), dtype=np.int32)
     @property
     def n_cams(self):
         return int(self.spatial_shape.shape[0])
@@ -134,7 +137,7 @@ class DeviceFeatures:
     def descriptor(self) -> L.Features:
         return L.Features(_ptr(self.table), _DTYPES[self.table.dtype], int(self.table.shape[0]), self.n_cams,
                           self.n_levels, self.channels, 0, int(self.table.shape[1]), _ptr(self.spatial_shape),
-                          _ptr(self.scale_start_index))
+                          _ptr(self.scale_start_index), ctypes.c_void_p(self._shape_host.ctypes.data))
 
     @classmethod
     def from_grids(cls, grids, device="cuda", dtype=torch.float32):

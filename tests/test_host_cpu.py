@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 def test_status_strings_and_abi_version():
     from paper_2601_10819_b200 import _lib
 
-    assert _lib.lib().msda_abi_version() == 1
+    assert _lib.lib().msda_abi_version() == 2
     assert "zero" in _lib.status_string(_lib.MSDA_ZERO_WEIGHT_SUM)
     assert _lib.status_string(_lib.MSDA_OK) == "ok"
 
