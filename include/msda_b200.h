@@ -198,7 +198,9 @@ int32_t msda_oae_pool(const msda_features_t *feat, int32_t n_queries, const floa
 size_t msda_oae_workspace_size(int32_t n_queries, int32_t n_cams, int32_t channels);
 
 /* Visible fraction of every object in every camera (visibility.py:46-115):
- * objects [n_objects, 7] f64 (x, y, z, w, l, h, yaw), image_wh [n_cams, 2]
+ * objects [n_objects, 9] f64 (x, y, z, w, l, h, yaw, cos(yaw), sin(yaw)) with
+ * cos / sin from the HOST libm (Python's math.cos / math.sin in rot_z,
+ * geometry.py:50-53: the counts are then bit-exact), image_wh [n_cams, 2]
  * int32, grid samples per axis (reference default 64).  Out: visibility
  * [n_cams, n_objects] f32 in [0, 1], fully_behind [n_cams, n_objects] (no box
  * corner in front of the camera -> visibility 0).  These are the v_i that
@@ -211,8 +213,9 @@ int32_t msda_visibility(const msda_cameras_t *cams, const int32_t *image_wh, int
 /* Feature painting (simulator.py:249-289) straight into
  * the channel-last table: grid (cam, level) has spatial_shape (H, W) =
  * (ceil(img_h / stride), ceil(img_w / stride)) (simulator.py:252-253) and
- * starts at scale_start_index.  entities [n_objects + n_occluders, 7] f64
- * (x, y, z, w, l, h, yaw): moving objects (signatures [n_objects, C] f64)
+ * starts at scale_start_index.  entities [n_objects + n_occluders, 9] f64
+ * (x, y, z, w, l, h, yaw, cos(yaw), sin(yaw), the trig from the host libm as
+ * for msda_visibility): moving objects (signatures [n_objects, C] f64)
  * then occluders (paint nothing).  A cell takes the signature of the nearest
  * entity whose projected rect (visibility.py:46-65) covers its centre.
  * background [rows, C] f64 (the reference's numpy draw: bit-identical

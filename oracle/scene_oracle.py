@@ -84,6 +84,28 @@ def projected_rect(K, R, t, state, eps=1e-6):
     return (min(us), max(us), min(vs), max(vs), float(np.mean(ds)))
 
 
+def visible_fraction(K, R, t, width, height, objects, target, grid=64):
+    """visibility.py:68-115 for one (camera, target object): (value, fully_behind)."""
+    rect = projected_rect(K, R, t, objects[target])
+    if rect is None:
+        return 0.0, True
+    blockers = []
+    for o, obj in enumerate(objects):
+        if o == target:
+            continue
+        br = projected_rect(K, R, t, obj)
+        if br is not None and br[4] < rect[4]:
+            blockers.append(br)
+    steps = (np.arange(grid, dtype=float) + 0.5) / grid
+    us = rect[0] + steps * (rect[1] - rect[0])
+    vs = rect[2] + steps * (rect[3] - rect[2])
+    uu, vv = np.meshgrid(us, vs)
+    visible = (uu >= 0.0) & (uu < width) & (vv >= 0.0) & (vv < height)
+    for br in blockers:
+        visible &= ~((br[0] <= uu) & (uu <= br[1]) & (br[2] <= vv) & (vv <= br[3]))
+    return float(np.count_nonzero(visible)) / float(grid * grid), False
+
+
 def paint_grid(K, R, t, image_wh, stride, entities, signatures, background):
     """simulator.py:249-289 for one (camera, level) grid.
 

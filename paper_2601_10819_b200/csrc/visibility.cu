@@ -13,7 +13,14 @@
 //                    grid^2 sample points at cell centres of the target rect
 //                    are visible when inside [0, W) x [0, H) and outside every
 //                    blocker rect (closed bounds); the count is block-reduced.
-// The f64 arithmetic is separately rounded (__dmul_rn/__dadd_rn) like numpy's.
+// Bit-exact with the reference on the same host arithmetic: cos / sin of the
+// yaw come from the caller (Python's math.cos / math.sin in rot_z,
+// geometry.py:50-53 — the device libm differs in the last bit); the two
+// numpy matrix products follow the OpenBLAS (SkylakeX) kernels numpy calls,
+// measured here bit for bit: `local @ rot_z(yaw).T` (geometry.py:205) is the
+// FMA chain k = 0, 1, 2 per output, `R @ p` (geometry.py:176) is
+// fma(R2, p2, fma(R0, p0, R1 * p1)); the rest is separately rounded
+// (__dmul_rn / __dadd_rn / __ddiv_rn) like numpy's scalar ops.
 #include <algorithm>
 
 #include "msda_common.cuh"
@@ -32,23 +39,24 @@ struct VisArgs {
   const double* R;    // [cams, 9]
   const double* T;    // [cams, 3]
   const int32_t* wh;  // [cams, 2] image width, height
-  const double* obj;  // [n_obj, 7] x, y, z, w, l, h, yaw
+  const double* obj;  // [n_obj, 9] x, y, z, w, l, h, yaw, cos(yaw), sin(yaw) (host libm)
   int32_t cams, n_obj, grid;
   Rect* rects;        // [cams, n_obj]
   float* vis;         // [cams, n_obj]
   uint8_t* behind;    // [cams, n_obj]
 };
 
+// one row of numpy's `R @ p` for a 3x3 R (OpenBLAS dgemv order)
 __device__ __forceinline__ double dot3(const double* r, double x, double y, double z) {
-  return __dadd_rn(__dadd_rn(__dmul_rn(r[0], x), __dmul_rn(r[1], y)), __dmul_rn(r[2], z));
+  return __fma_rn(r[2], z, __fma_rn(r[0], x, __dmul_rn(r[1], y)));
 }
 
 __global__ void rect_kernel(VisArgs a) {
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= (int64_t)a.cams * a.n_obj) return;
   const int cam = (int)(id / a.n_obj), o = (int)(id % a.n_obj);
-  const double* s = a.obj + (int64_t)o * 7;
-  const double c = cos(s[6]), sn = sin(s[6]);
+  const double* s = a.obj + (int64_t)o * 9;
+  const double c = s[7], sn = s[8];
   const double hl = s[4] / 2.0, hw = s[3] / 2.0, hh = s[5] / 2.0;
   const double* R = a.R + cam * 9;
   const double* T = a.T + cam * 3;
@@ -58,10 +66,11 @@ __global__ void rect_kernel(VisArgs a) {
   int n = 0;
   for (int i = 0; i < 8; ++i) {
     const double lx = (i & 1) ? hl : -hl, ly = (i & 2) ? hw : -hw, lz = (i & 4) ? hh : -hh;
-    // local @ rot_z(yaw)^T + centre
-    const double px = __dadd_rn(__dadd_rn(__dmul_rn(lx, c), __dmul_rn(ly, -sn)), s[0]);
-    const double py = __dadd_rn(__dadd_rn(__dmul_rn(lx, sn), __dmul_rn(ly, c)), s[1]);
-    const double pz = __dadd_rn(lz, s[2]);
+    // local @ rot_z(yaw)^T + centre: per output the FMA chain over the rows
+    // of rot_z = [[c, -s, 0], [s, c, 0], [0, 0, 1]] (OpenBLAS dgemm order)
+    const double px = __dadd_rn(__fma_rn(lz, 0.0, __fma_rn(ly, -sn, __dmul_rn(lx, c))), s[0]);
+    const double py = __dadd_rn(__fma_rn(lz, 0.0, __fma_rn(ly, c, __dmul_rn(lx, sn))), s[1]);
+    const double pz = __dadd_rn(__fma_rn(lz, 1.0, __fma_rn(ly, 0.0, __dmul_rn(lx, 0.0))), s[2]);
     const double xc = __dadd_rn(dot3(R, px, py, pz), T[0]);
     const double yc = __dadd_rn(dot3(R + 3, px, py, pz), T[1]);
     const double zc = __dadd_rn(dot3(R + 6, px, py, pz), T[2]);

@@ -371,6 +371,17 @@ def oae_pool(feats: DeviceFeatures, anchors, learned_offsets, cameras: Cameras, 
     return out, occl.bool()
 
 
+def _boxes_with_trig(boxes):
+    """[n, 7] (x, y, z, w, l, h, yaw) -> [n, 9] f64 with cos(yaw), sin(yaw)
+    from Python's math module: the values rot_z uses (geometry.py:50-53), so
+    the device corner arithmetic sees the reference's bits (C ABI contract)."""
+    import math
+
+    b = np.asarray(boxes.cpu() if isinstance(boxes, torch.Tensor) else boxes, dtype=np.float64).reshape(-1, 7)
+    trig = np.array([[math.cos(y), math.sin(y)] for y in b[:, 6]], dtype=np.float64).reshape(-1, 2)
+    return torch.from_numpy(np.ascontiguousarray(np.concatenate([b, trig], axis=1)))
+
+
 def visibility(cameras: Cameras, image_wh, objects, grid: int = 64):
     """Visible fraction of every object in every camera (visibility.py:46-115).
 
@@ -378,7 +389,7 @@ def visibility(cameras: Cameras, image_wh, objects, grid: int = 64):
     Returns (visibility [cams, n] f32, fully_behind [cams, n] bool).
     """
     dev = cameras.K.device
-    obj = torch.as_tensor(objects, dtype=torch.float64).reshape(-1, 7).to(dev).contiguous()
+    obj = _boxes_with_trig(objects).to(dev).contiguous()
     wh = torch.as_tensor(image_wh, dtype=torch.int32).reshape(-1, 2).to(dev).contiguous()
     n_cams, n_obj = int(cameras.K.shape[0]), int(obj.shape[0])
     if wh.shape[0] != n_cams:
@@ -427,7 +438,7 @@ class PaintScene:
             for m in range(n_levels):
                 start[c, m] = rows
                 rows += int(shape[c, m, 0] * shape[c, m, 1])
-        self.ent = torch.as_tensor(np.asarray(entities, dtype=np.float64).reshape(-1, 7)).to(dev).contiguous()
+        self.ent = _boxes_with_trig(entities).to(dev).contiguous()
         n_ent = int(self.ent.shape[0])
         if not 0 <= n_objects <= n_ent:
             raise ValueError("n_objects must be within the entity count")

@@ -268,6 +268,25 @@ def visibility_case():
                 vis[ci, oi] = sc.value
                 behind[ci, oi] = sc.fully_behind
         scenes.append((cams, objs, vis, behind))
+    # denser scenes (more, larger, overlapping boxes; other image sizes): many
+    # sample points fall near rect edges, where the projection's last bit decides
+    rng2 = np.random.default_rng(54)
+    for k in range(12):
+        size = [(640, 480), (704, 256), (1920, 1080)][k % 3]
+        cams = ring_cameras(2 + k % 5, size=size, focal=float(rng2.uniform(250, 900)), radius=float(rng2.uniform(6, 14)))
+        objs = []
+        for _ in range(10 + 2 * k):
+            objs.append([rng2.uniform(-4, 4), rng2.uniform(-4, 4), rng2.uniform(0.3, 1.5), rng2.uniform(0.3, 2.5),
+                         rng2.uniform(0.3, 3.0), rng2.uniform(0.5, 2.5), rng2.uniform(-math.pi, math.pi)])
+        states = [G.ObjectState3D(*o) for o in objs]
+        vis = np.zeros((len(cams), len(states)))
+        behind = np.zeros((len(cams), len(states)), dtype=bool)
+        for ci, cam in enumerate(cams):
+            for oi, st in enumerate(states):
+                sc = visible_fraction(cam, st, states, grid=64)
+                vis[ci, oi] = sc.value
+                behind[ci, oi] = sc.fully_behind
+        scenes.append((cams, objs, vis, behind))
     out = {}
     for k, (cams, objs, vis, behind) in enumerate(scenes):
         out[f"K{k}"] = np.array([[c.focal_x, c.focal_y, c.principal_x, c.principal_y] for c in cams])
@@ -276,6 +295,7 @@ def visibility_case():
         out[f"obj{k}"] = np.array(objs)
         out[f"vis{k}"] = vis
         out[f"behind{k}"] = behind
+        out[f"wh{k}"] = np.array([[c.width, c.height] for c in cams])
     return out
 
 
