@@ -697,9 +697,48 @@ def sparse4d_block(args, dev, smi_index):
         res["cases"][key] = case
         del feats, loc, w, out, ref
         torch.cuda.empty_cache()
+    res["cases"]["cfg1_project_f32"] = _project_case(dev, stream, flush_buf, reps, peak)
     res["block_s"] = time.time() - t_block
     res["clocks"] = clocks.stop()
     return res
+
+
+def _project_case(dev, stream, flush_buf, reps, peak, cams=6, Q=900, C=256, G=8, L=4):
+    """north_star subsystem 2: keypoint generation + projection fused
+    (msda_dense_project: f64 projection pre-pass, then the pipelined gather)
+    at the cfg1 shape, against the plain operator on host-projected inputs'
+    time; parity on 24 anchors vs the composed oracle (geometry.py:207-255 ->
+    project_point -> pixel_to_cell -> msda_reference per group), 1e-4."""
+    import torch
+
+    from oracle import msda_oracle as mo
+    from paper_2601_10819_b200 import ops
+    from tools import sparse4d_cases as s4
+
+    feats = s4.make_feats(cams, s4.CFG1_LEVELS, C, torch.float32, dev, seed=77)
+    K, R, T = s4.ring(cams)
+    camd = ops.Cameras(K, R, T, device=dev)
+    anchors = s4.anchors_for(Q, dev).unsqueeze(0)
+    offs = (torch.rand((6, 3), generator=torch.Generator().manual_seed(3)) * 2 - 1).to(dev)
+    strides = torch.tensor([4.0, 8.0, 16.0, 32.0], device=dev)
+    _, w = s4.make_dense_inputs(1, Q, 13, cams, L, G, dev, seed=78)
+    out = torch.empty((1, Q, C), device=dev)
+    fn = lambda: ops.msda_dense_project(feats, anchors, offs, camd, strides, w, dt=0.1, out=out)  # noqa: E731
+    ops.msda_dense_project(feats, anchors, offs, camd, strides, w, dt=0.1, out=out, check=True)
+    nq = 24
+    table, tiles, _ = s4.host_view(feats)
+    ref = mo.msda_project_groups(table, tiles, anchors[:, :nq].cpu().numpy(), offs.cpu().numpy(), K, R, T,
+                                 [4.0, 8.0, 16.0, 32.0], w[:, :nq].cpu().numpy(), L, False, 0.1)
+    err = float(np.abs(out[:, :nq].cpu().numpy() - ref).max() / max(1e-12, np.abs(ref).max()))
+    for _ in range(3):
+        fn()
+    cold = _time_events(fn, reps, stream, flush_buf)
+    warm = _time_events(fn, reps, stream)
+    return {"desc": "cfg1 shape with keypoints (7 fixed + 6 learned) generated and projected (f64) from 900 anchors "
+                    "through 6 ring cameras (704x256, f=300 px), fp32, FAST",
+            "path": "msda_dense_project: projection pre-pass + pipelined gather",
+            "latency_us": cold[len(cold) // 2] * 1e3, "warm_us": warm[len(warm) // 2] * 1e3,
+            "max_rel_err_vs_oracle_24_anchors": err, "tolerance": 1e-4, "within_tolerance": err <= 1e-4}
 
 
 def _cfg3_frame(feats, dev, stream, reps, Q, P, G, C, L, cams, layers=6):

@@ -439,3 +439,27 @@ def fuse(per_view, vis, memory, floor=1e-3):
     if n < 1e-12 or not np.isfinite(n):
         raise ValueError("cannot normalize a zero or non-finite vector")
     return raw / n, False
+
+
+def msda_project_groups(table, tiles, anchors, offsets, K, R, T, strides, wts, n_levels, normalize, dt):
+    """Fused projection oracle: generate_keypoints ->
+    motion_compensate -> project_point (behind-camera samples leave the plan)
+    -> pixel_to_cell per level -> msda_reference per channel group."""
+    bs, q_n = anchors.shape[:2]
+    g_n = wts.shape[-1]
+    c_n = table.shape[1]
+    cg = c_n // g_n
+    out = np.zeros((bs * q_n, c_n), dtype=np.float32)
+    cams = list(zip(K, R, T))
+    for b in range(bs):
+        plans = projection_plan(anchors[b].astype(np.float64), offsets.astype(np.float64), cams, strides,
+                                   None, dt=dt)
+        for q, samples in enumerate(plans):
+            for g in range(g_n):
+                pq = [(c, m, np.float32(u), np.float32(v), wts[b, q, p, c, m, g]) for c, m, u, v, p in samples]
+                offs, cam, lvl, uu, vv, ww = csr_from_per_query([pq])
+                sub = np.ascontiguousarray(table[:, g * cg:(g + 1) * cg])
+                if len(pq):
+                    r, _ = msda_exact(sub, tiles, n_levels, offs, cam, lvl, uu, vv, ww, normalize)
+                    out[b * q_n + q, g * cg:(g + 1) * cg] = r[0]
+    return out.reshape(bs, q_n, c_n)

@@ -595,6 +595,31 @@ cudaError_t launch_dense_offsets(int64_t* off, int64_t nq, int n, cudaStream_t s
   return cudaGetLastError();
 }
 
+// Projection pre-pass of the fused FAST path: one thread per (batch, anchor,
+// keypoint, camera) builds the keypoint (geometry.py:207-255, f64), projects
+// it (geometry.py:162-182, f64) and writes every level's cell coordinate
+// cell[((bq * P + p) * cams + cam) * L + l] = f32(pixel / stride_l - 0.5)
+// (features.py:45-47), or NaN when depth <= 1e-6 (the sample leaves the plan).
+__global__ void project_prepass_kernel(DenseArgs a, float2* cell) {
+  const int64_t n = (int64_t)a.bs * a.Q * a.P * a.cams;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int cam = (int)(i % a.cams);
+    const int64_t bqp = i / a.cams;
+    const int64_t bq = bqp / a.P;
+    const int p = (int)(bqp - bq * a.P);
+    double kp[3];
+    if (!anchor_keypoint(a.anchors + bq * 10, p, a.offsets, a.dt, kp) && cam == 0)
+      set_status(a.status, MSDA_OFFSET_RANGE, p);
+    double u, v;
+    const bool ok = project_point(a, cam, kp, u, v);
+    for (int l = 0; l < a.L; ++l) {
+      const double st = (double)a.strides[l];
+      cell[i * a.L + l] = ok ? make_float2((float)(u / st - 0.5), (float)(v / st - 0.5))
+                             : make_float2(__int_as_float(0x7fc00000), 0.0f);
+    }
+  }
+}
+
 // out[q, c] /= weight_sums[q, c / (C / G)] (camera-sharded partials after the all-reduce)
 __global__ void group_normalize_kernel(float* out, const float* wsum, int64_t n_q, int C, int G, DevStatus* st) {
   const int cpg = C / G;
@@ -719,6 +744,28 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
           const int64_t total = nq * a.C;
           const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
           group_normalize_kernel<<<blocks, 256, 0, s>>>(out, wsum_out ? wsum_out : scratch, nq, a.C, G, ew.status);
+          if (cudaGetLastError() != cudaSuccess) return MSDA_CUDA_ERROR;
+        }
+        return MSDA_OK;
+      }
+      if (e != cudaErrorNotSupported) return MSDA_CUDA_ERROR;
+    }
+    if (project) {  // projection pre-pass, then the pipelined gather on its pixel coordinates
+      float2* uv = reinterpret_cast<float2*>(ew.g_hi);  // the exact sort scratch (8 B per sample) is free in FAST
+      const int64_t n = nq * P * a.cams;
+      const int blocks = (int)std::min<int64_t>((n + 127) / 128, 148 * 32);
+      project_prepass_kernel<<<blocks, 128, 0, s>>>(a, uv);
+      if (cudaGetLastError() != cudaSuccess) return MSDA_CUDA_ERROR;
+      float* scratch = reinterpret_cast<float*>(ew.rec);
+      DenseFastSpec d{nullptr, w, Q, P, G, normalize, wsum_out, scratch, h2};
+      d.proj_cell = uv;
+      bool pending = false;
+      cudaError_t e = launch_gather_dense_fast(*f, d, ew.status, out, s, &pending);
+      if (e == cudaSuccess) {
+        if (pending) {
+          const int64_t total = nq * a.C;
+          const int nb = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+          group_normalize_kernel<<<nb, 256, 0, s>>>(out, wsum_out ? wsum_out : scratch, nq, a.C, G, ew.status);
           if (cudaGetLastError() != cudaSuccess) return MSDA_CUDA_ERROR;
         }
         return MSDA_OK;

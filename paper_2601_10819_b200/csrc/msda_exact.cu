@@ -336,6 +336,10 @@ struct GatherArgs {
   int32_t cps, n_split;
   int32_t n_lv;        // DENSE: levels [0, n_lv) of every camera
   int32_t accumulate;  // DENSE: always red.add into the zeroed totals (another kernel adds to them too)
+  // DENSE with fused projection: cell coordinates [q, P, cams, L] from the
+  // projection pre-pass (f32(pixel / stride_l - 0.5) in f64; NaN = behind the
+  // camera: outside every grid, weight 0) instead of loc
+  const float2* proj_cell;
 };
 
 __device__ __forceinline__ SampleRec ld_rec(const SampleRec* p) {
@@ -615,14 +619,23 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
         const int t = cam * a.n_levels + l;
         const int H = a.shape[2 * t], W = a.shape[2 * t + 1];
         const int64_t pc = (q * a.P + p) * a.n_cams + cam;
-        const float2 lp = __ldg(reinterpret_cast<const float2*>(a.loc) + pc);
-        const float uu = __fsub_rn(__fmul_rn(lp.x, (float)W), 0.5f);
-        const float vv = __fsub_rn(__fmul_rn(lp.y, (float)H), 0.5f);
+        float uu, vv;
+        bool valid = true;
+        if (a.proj_cell) {  // projected keypoint (geometry.py:162-182), cell = pixel / stride - 0.5
+          const float2 cl = a.proj_cell[pc * a.n_levels + l];
+          valid = !isnan(cl.x);
+          uu = valid ? cl.x : -4.0f;
+          vv = valid ? cl.y : -4.0f;
+        } else {
+          const float2 lp = __ldg(reinterpret_cast<const float2*>(a.loc) + pc);
+          uu = __fsub_rn(__fmul_rn(lp.x, (float)W), 0.5f);
+          vv = __fsub_rn(__fmul_rn(lp.y, (float)H), 0.5f);
+        }
         r = make_record(uu, vv, (q / a.q_per_batch) * a.rows_per_batch + a.start[t], H, W);
         const float* wp = a.w + (pc * a.n_levels + l) * a.n_groups;
 #pragma unroll
         for (int k = 0; k < GW; ++k)
-          if (k < a.n_groups) r_wg[k] = __ldg(wp + k);
+          if (k < a.n_groups) r_wg[k] = valid ? __ldg(wp + k) : 0.0f;  // behind the camera: out of the plan
       } else if constexpr (RAW) {
         const int64_t si = lo + s;
         int c = __ldg(a.cam + si), l = __ldg(a.lvl + si);
@@ -933,6 +946,7 @@ cudaError_t launch_gather_dense_fast(const msda_features_t& f, const DenseFastSp
   g.out = out;
   g.w = d.w;
   g.loc = d.loc;
+  g.proj_cell = d.proj_cell;
   g.P = d.P;
   g.q_per_batch = d.Q > 0 ? d.Q : 1;
   g.rows_per_batch = f.n_rows;
@@ -946,7 +960,7 @@ cudaError_t launch_gather_dense_fast(const msda_features_t& f, const DenseFastSp
   g.n_groups = G;
   g.cpg = cpg;
   if (reinterpret_cast<uintptr_t>(f.data) % 16 || (C * esz) % 16 || reinterpret_cast<uintptr_t>(out) % 16 ||
-      reinterpret_cast<uintptr_t>(d.loc) % 8)
+      (!d.proj_cell && reinterpret_cast<uintptr_t>(d.loc) % 8))
     return cudaErrorNotSupported;
   // a lane's channels must share one group, a query's channels span whole warps
   const int vec = f.dtype == MSDA_F32 ? 4 : 8;  // 16-B lanes

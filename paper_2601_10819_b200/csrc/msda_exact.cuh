@@ -43,6 +43,7 @@ struct DenseFastSpec {
   float* wsum_out;      // [batch * Q, G] or null
   float* wsum_scratch;  // [batch * Q, G] device scratch for split normalisation
   bool h2;              // FAST_H2: half2 accumulation per camera (f16 storage; other dtypes ignore it)
+  const float2* proj_cell = nullptr;  // fused projection: cells [batch * Q, P, cams, L] (NaN: behind), or null
   int32_t n_lv = 0;        // gather only levels [0, n_lv) (0: all)
   bool accumulate = false;  // out / wsum are zeroed by the caller: always red.add, the caller normalises
 };

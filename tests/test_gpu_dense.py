@@ -121,35 +121,18 @@ def _ring(n, radius=12.0, height=4.0, focal=300.0, size=(704, 256)):
     return np.array(Ks), np.array(Rs), np.array(ts)
 
 
-def _proj_oracle(table, tiles, anchors, offsets, K, R, T, strides, wts, n_levels, normalize, dt):
-    bs, q_n = anchors.shape[:2]
-    g_n = wts.shape[-1]
-    c_n = table.shape[1]
-    cg = c_n // g_n
-    out = np.zeros((bs * q_n, c_n), dtype=np.float32)
-    cams = list(zip(K, R, T))
-    for b in range(bs):
-        plans = mo.projection_plan(anchors[b].astype(np.float64), offsets.astype(np.float64), cams, strides,
-                                   None, dt=dt)
-        for q, samples in enumerate(plans):
-            for g in range(g_n):
-                pq = [(c, m, np.float32(u), np.float32(v), wts[b, q, p, c, m, g]) for c, m, u, v, p in samples]
-                offs, cam, lvl, uu, vv, ww = mo.csr_from_per_query([pq])
-                sub = np.ascontiguousarray(table[:, g * cg:(g + 1) * cg])
-                if len(pq):
-                    r, _ = mo.msda_exact(sub, tiles, n_levels, offs, cam, lvl, uu, vv, ww, normalize)
-                    out[b * q_n + q, g * cg:(g + 1) * cg] = r[0]
-    return out.reshape(bs, q_n, c_n)
-
-
-@pytest.mark.parametrize("normalize", [False, True])
-def test_dense_project_matches_composed_oracle(cuda_dev, normalize):
+@pytest.mark.parametrize("normalize,channels,groups", [(False, 64, 4), (True, 64, 4), (False, 256, 8),
+                                                      (True, 256, 8)])
+def test_dense_project_matches_composed_oracle(cuda_dev, normalize, channels, groups):
+    """Fused keypoints + projection (msda_dense_project) against the composed
+    oracle.  C = 256 takes the projection pre-pass + pipelined gather; C = 64
+    the anchor-major fused kernel."""
     import torch
 
     from paper_2601_10819_b200 import ops
 
     rng = np.random.default_rng(55)
-    cams, n_levels, channels, groups = 4, 4, 64, 4
+    cams, n_levels = 4, 4
     strides = [4.0, 8.0, 16.0, 32.0]
     grids = {}
     shape = np.zeros((cams, n_levels, 2), dtype=np.int32)
@@ -172,7 +155,7 @@ def test_dense_project_matches_composed_oracle(cuda_dev, normalize):
     wts = rng.uniform(0.01, 1.0, (1, q_n, 13, cams, n_levels, groups)).astype(np.float32)
     camd = ops.Cameras(K, R, T, device=cuda_dev)
     t = lambda a: torch.from_numpy(a).to(cuda_dev)  # noqa: E731
-    ref = _proj_oracle(table, tiles, anchors, offsets, K, R, T, strides, wts, n_levels, normalize, 0.1)
+    ref = mo.msda_project_groups(table, tiles, anchors, offsets, K, R, T, strides, wts, n_levels, normalize, 0.1)
     for prec in ("fast", "exact"):
         out = ops.msda_dense_project(feats, t(anchors), offsets, camd, strides, t(wts), dt=0.1, precision=prec,
                                      normalize=normalize, check=True).cpu().numpy()

@@ -32,6 +32,9 @@ def main():
     if args.json:
         Path(args.json).write_text(json.dumps(res))
     for key, c in res["cases"].items():
+        if "paths" not in c:
+            print(key, {k: v for k, v in c.items() if k not in ("desc",)})
+            continue
         for p, v in c["paths"].items():
             par = "bits" if v.get("bitwise_equal_to_oracle") else (
                 f"err {v['max_rel_err_vs_oracle']:.1e}" if "max_rel_err_vs_oracle" in v else "MISMATCH")

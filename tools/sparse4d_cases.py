@@ -10,6 +10,8 @@ across levels, weights softmax over (P * cams * L) of N(0, 1) logits per
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 import torch
 
@@ -85,3 +87,33 @@ def host_view(feats):
     cams, L = shape.shape[:2]
     tiles = [(int(start[c, m]), int(shape[c, m, 0]), int(shape[c, m, 1])) for c in range(cams) for m in range(L)]
     return table, tiles, shape
+
+
+def ring(cams, radius=12.0, height=4.0, focal=300.0, size=(704, 256)):
+    """Cameras on a ring looking at (0, 0, 0.9) (camera_looking_at, geometry.py:258-290, restated):
+    K [cams, 4] (fx, fy, cx, cy), R [cams, 3, 3], t [cams, 3] (SURVEY §8(d) projection runs)."""
+    Ks, Rs, ts = [], [], []
+    for i in range(cams):
+        ang = 2 * math.pi * i / cams
+        pos = np.array([radius * math.cos(ang), radius * math.sin(ang), height])
+        z = np.array([0.0, 0.0, 0.9]) - pos
+        z /= np.linalg.norm(z)
+        x = np.cross(z, [0.0, 0.0, 1.0])
+        x /= np.linalg.norm(x)
+        y = np.cross(z, x)
+        R = np.vstack([x, y, z])
+        Ks.append([focal, focal, size[0] / 2, size[1] / 2])
+        Rs.append(R)
+        ts.append(-R @ pos)
+    return np.array(Ks), np.array(Rs), np.array(ts)
+
+
+def anchors_for(Q, dev, seed=2):
+    """Anchors uniform in x, y in [-4, 4] m, z = 0.9, (w, l, h) = (0.6, 0.6, 1.8), yaw U(-pi, pi)."""
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    a = torch.zeros((Q, 10))
+    a[:, 0:2] = torch.rand((Q, 2), generator=g) * 8 - 4
+    a[:, 2] = 0.9
+    a[:, 3:6] = torch.tensor([0.6, 0.6, 1.8])
+    a[:, 6] = torch.rand(Q, generator=g) * 2 * math.pi - math.pi
+    return a.to(dev)
