@@ -790,6 +790,31 @@ DENSE_CONFIGS = {
 CFG1_LEVELS = [(64, 176), (32, 88), (16, 44), (8, 22)]
 
 
+def _nccl_debug_setup(rank):
+    """Before the process group exists: NCCL INFO logging into a per-rank
+    file, so the bench line can say which algorithms / NVLS NCCL set up."""
+    path = f"/tmp/msda_nccl.{os.getpid()}.{rank}.log"
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,TUNING,NVLS,GRAPH")
+    os.environ["NCCL_DEBUG_FILE"] = path
+    return path
+
+
+def _nccl_report(path):
+    import torch
+
+    rep = {"version": ".".join(map(str, torch.cuda.nccl.version())) if hasattr(torch.cuda, "nccl") else None,
+           "env": {k: os.environ[k] for k in ("NCCL_ALGO", "NCCL_PROTO", "NCCL_NVLS_ENABLE") if k in os.environ}}
+    try:
+        lines = Path(path).read_text(errors="replace").splitlines()
+    except OSError:
+        return {**rep, "log": "absent"}
+    nvls = [ln.split("NCCL INFO", 1)[-1].strip() for ln in lines if "NVLS" in ln or "nvls" in ln]
+    algo = [ln.split("NCCL INFO", 1)[-1].strip() for ln in lines if "Algo" in ln or "algorithm" in ln.lower()]
+    rep.update({"nvls_lines": nvls[:8], "algo_lines": algo[:8], "log_lines": len(lines)})
+    return rep
+
+
 def run_dense_scaling(args, cfg, rank, local_rank, world):
     """cfg5 sweep (strong scaling: 512 cameras in total whatever N is)."""
     import torch
@@ -800,6 +825,7 @@ def run_dense_scaling(args, cfg, rank, local_rank, world):
 
     dev, backend = rank_device(local_rank)
     torch.cuda.set_device(dev)
+    nccl_log = _nccl_debug_setup(rank) if (world > 1 and backend == "nccl") else None
     if world > 1:
         dist.init_process_group(backend, device_id=dev)
     Q, P, G, C, L = 900, 13, 8, 256, 4
@@ -818,6 +844,8 @@ def run_dense_scaling(args, cfg, rank, local_rank, world):
         w = torch.softmax(torch.randn((1, Q, P * n_cams * L, G), generator=gen, device=dev), dim=2)
         return loc, w.reshape(1, Q, P, n_cams, L, G).contiguous()
 
+    step_mode = "eager"
+    agg = None
     if cfg["shard"] == "stream":
         # this rank's scenes as ONE batched call: the scenes share the camera
         # and level geometry, so their tables stack as batch items [S, R, C]
@@ -845,11 +873,20 @@ def run_dense_scaling(args, cfg, rank, local_rank, world):
 
         def step():
             agg(loc, w, local_inputs=True, check=False)
+        if agg.transport == "collective":
+            # partial kernels + NCCL all-reduce + normalisation as one CUDA graph
+            try:
+                graph, _ = agg.capture(loc, w, normalize=True, local_inputs=True)
+                step, step_mode = graph.replay, "CUDA graph: partial + all-reduce + normalise"
+            except Exception as e:  # e.g. a gloo group (BENCH_SHARE_GPU): no capture, eager calls
+                log(f"[rank {rank}] capture unavailable ({type(e).__name__}: {e}); eager calls")
+                step = lambda: agg(loc, w, normalize=True, local_inputs=True, check=False)  # noqa: E731
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
+    torch.cuda.synchronize(dev)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for _ in range(args.steps):
@@ -857,19 +894,26 @@ def run_dense_scaling(args, cfg, rank, local_rank, world):
     b.record()
     torch.cuda.synchronize(dev)
     ms = a.elapsed_time(b) / args.steps
+    per_rank = [ms]
     if world > 1:
         t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        gathered = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(gathered, t)
+        per_rank = [float(x.item()) for x in gathered]
+        ms = max(per_rank)
     if rank == 0:
-        print(json.dumps({
+        line = {
             "metric": METRIC, "value": cfg["cams"] / (ms / 1e3), "unit": "camera-frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f16", "data": "synthetic (device RNG)",
             "config": {"workload": args.config, "desc": cfg["desc"], "queries": Q, "points": P, "groups": G,
                        "channels": C, "levels": CFG1_LEVELS},
-            "streams_at_30fps_6layers": int(cfg["cams"] / (30 * 6 * ms / 1e3))}), flush=True)
-    if cfg["shard"] == "camera":
+            "per_rank_ms": per_rank, "step_mode": step_mode, "backend": backend,
+            "streams_at_30fps_6layers": int(cfg["cams"] / (30 * 6 * ms / 1e3))}
+        if nccl_log:
+            line["nccl"] = _nccl_report(nccl_log)
+        print(json.dumps(line), flush=True)
+    if agg is not None:
         agg.close()
     if world > 1:
         dist.barrier()

@@ -134,69 +134,107 @@ class PeerExchange:
 class CameraShardedAggregation:
     """Sparse4D deformable aggregation of one scene with cameras across ranks.
 
-    ``local_fn(loc, weights)`` aggregates this rank's cameras without
-    normalisation and returns ``[bs, Q, C]`` float32 — or ``(out, weight_sums
-    [bs, Q, G])``.  On GPUs it is the C-ABI ``msda_dense_partial`` bound to
-    the rank's feature table and ``normalize_fn`` is ``msda_dense_normalize``
-    (see :meth:`for_device_features`), so no arithmetic runs outside the
-    library; the CPU tests pass a numpy stand-in and fall back to torch.
+    Device path (:meth:`for_device_features`): ``partial_into(loc, weights,
+    num, wsum)`` is the C-ABI ``msda_dense_partial`` writing this rank's
+    un-normalised numerators ``num [bs*Q, C]`` and per-(anchor, group)
+    weight sums ``wsum [bs*Q, G]`` straight into two views of ONE contiguous
+    buffer ``[bs*Q*C | bs*Q*G]``, so a single all-reduce sums both (no
+    staging copy), then ``normalize_fn`` (``msda_dense_normalize``) divides in
+    place — no arithmetic outside the library.  :meth:`capture` records
+    partial kernels + NCCL all-reduce + normalisation as one CUDA graph.
+
+    CPU tests pass ``local_fn(loc, weights)`` returning ``[bs, Q, C]`` (or
+    ``(out, weight_sums)``), copied into the same buffer, with a torch
+    normalisation fallback.
     """
 
     n_cams: int
-    local_fn: Callable
+    local_fn: Callable | None = None
     group: object = None
     normalize_fn: Callable | None = None
     transport: str = "collective"  # or "peer": PeerExchange over NVLink (GPU ranks, <= 8)
+    partial_into: Callable | None = None
 
     def __post_init__(self):
         if self.transport not in ("collective", "peer"):
             raise ValueError(f"unknown transport {self.transport!r}")
+        if self.local_fn is None and self.partial_into is None:
+            raise ValueError("local_fn or partial_into is required")
         self._peer = None
+        self._buf = None
         self.rank = dist.get_rank(self.group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(self.group) if dist.is_initialized() else 1
         self.cam_lo, self.cam_hi = camera_range(self.n_cams, self.rank, self.world)
+
+    def _packed(self, rows, c_n, g_n, device):
+        n = rows * (c_n + g_n)
+        if self._buf is None or self._buf.numel() != n or self._buf.device != torch.device(device):
+            self._buf = torch.empty(n, dtype=torch.float32, device=device)
+        return self._buf, self._buf[:rows * c_n].view(rows, c_n), self._buf[rows * c_n:].view(rows, g_n)
 
     def __call__(self, sampling_location, weights, normalize: bool = False, local_inputs: bool = False,
                  check: bool = True):
         """sampling_location [bs, Q, P, cams, 2], weights [bs, Q, P, cams, L, G]
         for ALL cameras (each rank slices its own) or, with ``local_inputs``,
         already restricted to this rank's camera range; returns [bs, Q, C]."""
+        out = self._run(sampling_location, weights, normalize, local_inputs, check)
+        return out.clone()
+
+    def _run(self, sampling_location, weights, normalize, local_inputs, check=True):
         if local_inputs:
             loc, wts = sampling_location, weights
         else:
             loc = sampling_location[:, :, :, self.cam_lo:self.cam_hi].contiguous()
             wts = weights[:, :, :, self.cam_lo:self.cam_hi].contiguous()
-        res = self.local_fn(loc, wts)
-        part, wsum = res if isinstance(res, tuple) else (res, None)
-        bs, q_n, c_n = part.shape
-        g_n = weights.shape[-1]
+        bs, q_n = int(loc.shape[0]), int(loc.shape[1])
+        g_n = int(weights.shape[-1])
+        rows = bs * q_n
+        if self.partial_into is not None:
+            c_n = self.channels
+            buf, num, wsum = self._packed(rows, c_n, g_n, loc.device)
+            self.partial_into(loc, wts, num, wsum)
+        else:  # CPU stand-in
+            res = self.local_fn(loc, wts)
+            part, ws_ = res if isinstance(res, tuple) else (res, None)
+            c_n = int(part.shape[-1])
+            buf, num, wsum = self._packed(rows, c_n, g_n, part.device)
+            num.copy_(part.reshape(rows, c_n))
+            if ws_ is None:  # the weight sums of this rank's cameras
+                ws_ = wts.sum(dim=(2, 3, 4), dtype=torch.float32)
+            wsum.copy_(ws_.reshape(rows, g_n))
         if self.transport == "peer":
-            if wsum is None:
-                wsum = wts.sum(dim=(2, 3, 4), dtype=torch.float32).to(part.device)
             px = self._peer
-            if px is None or (px.rows, px.channels, px.groups) != (bs * q_n, c_n, g_n):
+            if px is None or (px.rows, px.channels, px.groups) != (rows, c_n, g_n):
                 if px is not None:
                     px.close()
-                px = self._peer = PeerExchange(bs * q_n, c_n, g_n, part.device, self.group)
-            return px.allreduce_normalize(part, wsum, normalize, check=check).reshape(bs, q_n, c_n)
-        if normalize:
-            if wsum is None:  # CPU stand-in: the weight sums of this rank's cameras
-                wsum = wts.sum(dim=(2, 3, 4), dtype=torch.float32).to(part.device)  # [bs, Q, G]
-            # one all-reduce of [bs*Q, C + G]: numerators and weight sums together
-            buf = torch.cat([part.reshape(bs * q_n, c_n), wsum.reshape(bs * q_n, g_n)], dim=1)
-        else:
-            buf = part.reshape(bs * q_n, c_n)
-        if self.world > 1:
-            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
+                px = self._peer = PeerExchange(rows, c_n, g_n, num.device, self.group)
+            return px.allreduce_normalize(num, wsum, normalize, check=check).reshape(bs, q_n, c_n)
+        if self.world > 1:  # one all-reduce of the numerators (+ the weight sums when normalising)
+            dist.all_reduce(buf if normalize else num.view(-1), op=dist.ReduceOp.SUM, group=self.group)
         if not normalize:
-            return buf.reshape(bs, q_n, c_n)
-        out = buf[:, :c_n].contiguous()
-        ws = buf[:, c_n:].contiguous()
+            return num.reshape(bs, q_n, c_n)
         if self.normalize_fn is not None:
-            return self.normalize_fn(out, ws).reshape(bs, q_n, c_n)
-        if bool((ws == 0).any()):
+            return self.normalize_fn(num, wsum, check=check).reshape(bs, q_n, c_n)
+        if bool((wsum == 0).any()):
             raise ValueError("an anchor's weights sum to zero, cannot renormalize")
-        return (out.reshape(bs, q_n, g_n, c_n // g_n) / ws.reshape(bs, q_n, g_n, 1)).reshape(bs, q_n, c_n)
+        return (num.reshape(rows, g_n, c_n // g_n) / wsum.reshape(rows, g_n, 1)).reshape(bs, q_n, c_n)
+
+    def capture(self, sampling_location, weights, normalize: bool = False, local_inputs: bool = True):
+        """One call — partial kernels, NCCL all-reduce, normalisation —
+        captured as a CUDA graph over the given (static) input tensors: write
+        new inputs into them and ``replay()``.  Returns (graph, out): ``out``
+        [bs, Q, C] is the graph's output buffer, rewritten by every replay."""
+        if self.partial_into is None or self.transport != "collective":
+            raise ValueError("capture needs the device path and the collective transport")
+        self._run(sampling_location, weights, normalize, local_inputs, check=True)  # warm-up: comm, workspace
+        torch.cuda.synchronize(sampling_location.device)
+        side = torch.cuda.Stream(sampling_location.device)
+        side.wait_stream(torch.cuda.current_stream(sampling_location.device))
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side):
+            out = self._run(sampling_location, weights, normalize, local_inputs, check=False)
+        torch.cuda.current_stream(sampling_location.device).wait_stream(side)
+        return graph, out
 
     @classmethod
     def for_device_features(cls, n_cams, local_feats, precision="fast", group=None, transport="collective"):
@@ -205,10 +243,19 @@ class CameraShardedAggregation:
         the peer-memory exchange (``PeerExchange``)."""
         from . import ops
 
-        def local(loc, wts):
-            return ops.deformable_aggregation_partial(local_feats, loc, wts, precision=precision)
+        agg = cls(n_cams, None, group, ops.normalize_groups, transport, lambda *a: None)
+        agg.bind_features(local_feats, precision)
+        return agg
 
-        return cls(n_cams, local, group, ops.normalize_groups, transport)
+    def bind_features(self, local_feats, precision="fast"):
+        """(Re)bind the device path to this rank's feature table (a new frame)."""
+        from . import ops
+
+        def partial_into(loc, wts, num, wsum):
+            ops.deformable_aggregation_partial(local_feats, loc, wts, precision=precision, out=num, weight_sums=wsum)
+
+        self.partial_into = partial_into
+        self.channels = local_feats.channels
 
     def close(self):
         if self._peer is not None:

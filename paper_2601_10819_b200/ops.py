@@ -255,11 +255,13 @@ class Cameras:
         return cls(K, R, t, device)
 
 
-def deformable_aggregation_partial(feats: DeviceFeatures, sampling_location, weights, precision="fast"):
+def deformable_aggregation_partial(feats: DeviceFeatures, sampling_location, weights, precision="fast", out=None,
+                                   weight_sums=None):
     """Un-normalised FAST aggregation of ``feats``' cameras plus the
     per-(query, group) weight sums: the partials a camera-sharded rank
     all-reduces (C ABI ``msda_dense_partial``).  Returns (out [bs, Q, C],
-    weight_sums [bs, Q, G])."""
+    weight_sums [bs, Q, G]); ``out`` / ``weight_sums`` may be given (e.g. two
+    views of one buffer that a single all-reduce then sums)."""
     dev = feats.table.device
     loc = sampling_location.to(device=dev, dtype=torch.float32).contiguous()
     wts = weights.to(device=dev, dtype=torch.float32).contiguous()
@@ -270,8 +272,14 @@ def deformable_aggregation_partial(feats: DeviceFeatures, sampling_location, wei
         raise ValueError("sampling_location [bs, Q, P, cams, 2] and weights [bs, Q, P, cams, L, G] expected")
     if bs != feats.table.shape[0]:  # the C ABI takes the batch from the feature descriptor
         raise ValueError("batch of the feature table and sampling_location differ")
-    out = torch.empty((bs, q_n, feats.channels), dtype=torch.float32, device=dev)
-    wsum = torch.empty((bs, q_n, g_n), dtype=torch.float32, device=dev)
+    if out is None:
+        out = torch.empty((bs, q_n, feats.channels), dtype=torch.float32, device=dev)
+    if weight_sums is None:
+        weight_sums = torch.empty((bs, q_n, g_n), dtype=torch.float32, device=dev)
+    if (out.numel() != bs * q_n * feats.channels or weight_sums.numel() != bs * q_n * g_n or not out.is_contiguous()
+            or not weight_sums.is_contiguous() or out.dtype != torch.float32 or weight_sums.dtype != torch.float32):
+        raise ValueError("out [bs, Q, C] and weight_sums [bs, Q, G] must be contiguous float32")
+    wsum = weight_sums
     lib = L.lib()
     ws = WORKSPACE.get(dev, lib.msda_dense_workspace_size(bs, q_n, p_n, feats.n_cams, feats.n_levels, g_n,
                                                           feats.channels))
@@ -280,7 +288,7 @@ def deformable_aggregation_partial(feats: DeviceFeatures, sampling_location, wei
                                   _ptr(out), _ptr(wsum), _ptr(ws), ws.numel(), _stream(dev))
     if code != L.MSDA_OK:
         raise_for_status(code, -1, "deformable_aggregation_partial")
-    return out, wsum
+    return out.reshape(bs, q_n, feats.channels), wsum.reshape(bs, q_n, g_n)
 
 
 def normalize_groups(out, weight_sums, check=True):

@@ -67,7 +67,7 @@ def _worker(rank, world, port, cams, result_dir):
             if agg is None:
                 agg = CameraShardedAggregation.for_device_features(cams, feats, transport="peer")
             else:
-                agg.local_fn = (lambda f: (lambda l_, w_: ops.deformable_aggregation_partial(f, l_, w_)))(feats)
+                agg.bind_features(feats)
             t = lambda a: torch.from_numpy(a).to(dev)  # noqa: E731
             full_table, full_tiles = mo.pack_grids(grids, cams, 4)
             for normalize in (True, False):
