@@ -777,6 +777,11 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
     return e == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
   }
   if (precision == MSDA_EXACT_HALF && f->dtype != MSDA_F16) return MSDA_BAD_ARG;
+  if (precision == MSDA_EXACT && !normalize && !project) {  // one fused pass: runs ranked in the gather warp
+    const cudaError_t e = launch_dense_exact_fused(*f, loc, w, Q, P, G, out, s);
+    if (e == cudaSuccess) return MSDA_OK;
+    if (e != cudaErrorNotSupported) return MSDA_CUDA_ERROR;
+  }
   {  // EXACT, one pass for every group (bit-identical to the per-group plans below)
     const int n = P * a.cams * a.L;
     const size_t smem = (size_t)n * 9;

@@ -353,32 +353,6 @@ __device__ __forceinline__ SampleRec ld_rec(const SampleRec* p) {
   return r;
 }
 
-// acc[e] += wn * ((c0*w0 + c1*w1) + (c2*w2 + c3*w3)), two channels per FFMA2,
-// every product and sum rounded once (x*y + -0 == round(x*y); x*1 + y ==
-// round(x + y)).
-template <int VEC>
-__device__ __forceinline__ void exact_accumulate(float* acc, const float (*c)[VEC], const float4 iw, const float wn,
-                                                 const float2 one2, const float2 nz2) {
-  static_assert(VEC % 2 == 0, "pairs");
-  const float2 w0 = make_float2(iw.x, iw.x), w1 = make_float2(iw.y, iw.y);
-  const float2 w2 = make_float2(iw.z, iw.z), w3 = make_float2(iw.w, iw.w);
-  const float2 ws = make_float2(wn, wn);
-#pragma unroll
-  for (int e = 0; e < VEC; e += 2) {
-    const float2 a = __ffma2_rn(make_float2(c[0][e], c[0][e + 1]), w0, nz2);
-    const float2 b = __ffma2_rn(make_float2(c[1][e], c[1][e + 1]), w1, nz2);
-    const float2 d = __ffma2_rn(make_float2(c[2][e], c[2][e + 1]), w2, nz2);
-    const float2 f = __ffma2_rn(make_float2(c[3][e], c[3][e + 1]), w3, nz2);
-    const float2 ab = __ffma2_rn(a, one2, b);
-    const float2 df = __ffma2_rn(d, one2, f);
-    const float2 t = __ffma2_rn(ab, one2, df);
-    const float2 tw = __ffma2_rn(t, ws, nz2);
-    const float2 r = __ffma2_rn(tw, one2, make_float2(acc[e], acc[e + 1]));
-    acc[e] = r.x;
-    acc[e + 1] = r.y;
-  }
-}
-
 template <int VEC>
 __device__ __forceinline__ void half_accumulate(__half2* acch, const void* const* cvp, const float4 iw, const float wn) {
   const __half2 hw0 = __float2half2_rn(iw.x), hw1 = __float2half2_rn(iw.y);
@@ -478,21 +452,6 @@ __global__ void __launch_bounds__(256) gather_exact_kernel(GatherArgs a) {
 // query's records are staged 32 at a time (one coalesced load per lane, read
 // back as warp broadcasts), fetched one batch ahead.  Registers stay low, so
 // the ring depth — not the register file — sets the bytes in flight per SM.
-
-template <int BYTES>
-__device__ __forceinline__ void cp_async_zfill(uint32_t dst, const void* src, bool valid) {
-  const int n = valid ? BYTES : 0;
-  if constexpr (BYTES == 16) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(n));
-  } else {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(dst), "l"(src), "n"(BYTES), "r"(n));
-  }
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N));
-}
 
 template <int BYTES, int D, int GW = 1>
 struct PipeSmem {

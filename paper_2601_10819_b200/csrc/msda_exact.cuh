@@ -62,4 +62,10 @@ int dense_staged_fine_levels(const msda_features_t& f, int G, int P);
 cudaError_t launch_dense_coarse(const msda_features_t& f, const DenseFastSpec& d, int n_fine, float* out,
                                 float* wsum, cudaStream_t stream);
 
+// Dense EXACT without normalisation in one pass: the gather warp ranks each
+// (camera, level) run itself (msda_dense_exact.cu).  cudaErrorNotSupported
+// when the shape does not fit (the caller takes the two-pass path).
+cudaError_t launch_dense_exact_fused(const msda_features_t& f, const float* loc, const float* w, int Q, int P, int G,
+                                     float* out, cudaStream_t stream);
+
 }  // namespace msda

@@ -403,7 +403,8 @@ def test_dense_zero_weight_sum_raises(cuda_dev, cams, precision):
     (16, [(270, 480), (135, 240), (68, 120), (34, 60)], "float32"),  # cfg2 shape: 4 camera groups, maps >> L2
     (32, [(64, 176), (32, 88), (16, 44), (8, 22)], "bfloat16"),    # cfg4 MSDA part (staged coarse levels)
     (64, [(64, 176), (32, 88), (16, 44), (8, 22)], "float16")])    # cfg3 per layer (staged coarse levels)
-def test_dense_full_size_vs_c_oracle(c_oracle, cuda_dev, cams, levels, dt):
+@pytest.mark.parametrize("normalize", [True, False])
+def test_dense_full_size_vs_c_oracle(c_oracle, cuda_dev, cams, levels, dt, normalize):
     """BASELINE shapes at full size (900 anchors, 13 points, C = 256, G = 8),
     normalised, each path against the per-group C oracle (SURVEY §8(c):
     msda_reference on each group's channel slice) on the features the GPU
@@ -428,21 +429,25 @@ def test_dense_full_size_vs_c_oracle(c_oracle, cuda_dev, cams, levels, dt):
     loc = torch.from_numpy(loc_np).to(cuda_dev)
     seen = feats.table[0].float().cpu().numpy()
     tiles = [(int(start[c, m]), h, w) for c in range(cams) for m, (h, w) in enumerate(levels)]
-    ref = c_oracle.msda_dense_groups_c(seen, tiles, shape, loc_np, wts.cpu().numpy(), 4, normalize=True)
+    ref = c_oracle.msda_dense_groups_c(seen, tiles, shape, loc_np, wts.cpu().numpy(), 4, normalize=normalize)
     del seen
     scale = float(np.abs(ref).max())
-    exact = ops.deformable_aggregation(feats, None, None, loc, wts, precision="exact", normalize=True, check=True)
+    exact = ops.deformable_aggregation(feats, None, None, loc, wts, precision="exact", normalize=normalize,
+                                       check=True)
     assert exact.cpu().numpy().tobytes() == ref.tobytes()
-    fast = ops.deformable_aggregation(feats, None, None, loc, wts, precision="fast", normalize=True, check=True)
+    fast = ops.deformable_aggregation(feats, None, None, loc, wts, precision="fast", normalize=normalize,
+                                      check=True)
     assert float(np.abs(fast.cpu().numpy() - ref).max()) <= 1e-4 * scale
     if dt == "float16":
-        h2 = ops.deformable_aggregation(feats, None, None, loc, wts, precision="fast_h2", normalize=True, check=True)
+        h2 = ops.deformable_aggregation(feats, None, None, loc, wts, precision="fast_h2", normalize=normalize,
+                                        check=True)
         assert float(np.abs(h2.cpu().numpy() - ref).max()) <= 1e-2 * max(1.0, scale)
 
 
-@pytest.mark.parametrize("dt,precision", [("float32", "exact"), ("float16", "exact"), ("float32", "fast"),
-                                          ("float16", "fast_h2"), ("bfloat16", "fast")])
-def test_dense_run_to_run(cuda_dev, dt, precision):
+@pytest.mark.parametrize("dt,precision,normalize", [("float32", "exact", True), ("float16", "exact", False),
+                                                    ("float32", "fast", True), ("float16", "fast_h2", False),
+                                                    ("bfloat16", "fast", True), ("bfloat16", "exact", False)])
+def test_dense_run_to_run(cuda_dev, dt, precision, normalize):
     """Determinism contract: EXACT is run-to-run
     bit-identical (one sequential chain per (query, channel)); FAST / FAST_H2
     add camera-group and level partials with red.add in whatever order the
@@ -461,7 +466,7 @@ def test_dense_run_to_run(cuda_dev, dt, precision):
     feats = ops.DeviceFeatures(table, torch.from_numpy(shape), torch.from_numpy(start.astype(np.int64)))
     loc = torch.from_numpy(rng.uniform(0, 1, (1, Q, P, cams, 2)).astype(np.float32)).to(cuda_dev)
     wts = torch.from_numpy(rng.uniform(0.01, 1, (1, Q, P, cams, 4, G)).astype(np.float32)).to(cuda_dev)
-    outs = [ops.deformable_aggregation(feats, None, None, loc, wts, precision=precision, normalize=True,
+    outs = [ops.deformable_aggregation(feats, None, None, loc, wts, precision=precision, normalize=normalize,
                                        check=True).cpu().numpy() for _ in range(3)]
     if precision == "exact":
         assert outs[0].tobytes() == outs[1].tobytes() == outs[2].tobytes()
