@@ -664,8 +664,14 @@ def sparse4d_block(args, dev, smi_index):
                 "levels": [list(x) for x in levels], "algorithmic_bytes": ab,
                 "l2": "flushed per call" if feats.table.numel() * esize < 2 * L2_BYTES else "table larger than L2",
                 "oracle_s": oracle_s, "paths": {}}
+        n_fine = s4.staged_fine_levels(levels, dtype)
         for prec in precs:
             fn = (lambda p=prec: ops.deformable_aggregation(feats, None, None, loc, w, precision=p, out=out))  # noqa
+            # bytes that cross L2 -> SM as corner gathers: every level, or only
+            # the fine ones when the coarse levels come from TMA-staged smem
+            staged = n_fine is not None and prec != "exact"
+            l2_bytes = (sum(ab["gathered_corner_bytes_per_level"][:n_fine]) if staged
+                        else ab["gathered_corner_bytes"])
             ops.deformable_aggregation(feats, None, None, loc, w, precision=prec, out=out, check=True)
             got = out.cpu().numpy()
             err = float(np.abs(got - ref).max() / max(1e-12, scale))
@@ -688,10 +694,12 @@ def sparse4d_block(args, dev, smi_index):
                 "streams_at_30fps_6layers": int(cams / (30 * 6 * med_c / 1e3)),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak},
-                "l2_gather": {"bytes": ab["gathered_corner_bytes"],
-                              "achieved_gbs": ab["gathered_corner_bytes"] / (med_c / 1e3) / 1e9,
-                              "frac_of_ceiling": (ab["gathered_corner_bytes"] / (med_c / 1e3) / 1e9 / ceiling)
-                              if ceiling else None}}
+                "path": ("levels 2-3 from TMA-staged shared memory (staged_coarse_kernel) + levels 0-1 by the "
+                         "pipelined gather" if staged else
+                         "fused one-pass exact gather" if prec == "exact" else "anchor-major pipelined gather"),
+                "l2_gather": {"bytes": l2_bytes, "levels": f"0-{n_fine - 1}" if staged else "all",
+                              "achieved_gbs": l2_bytes / (med_c / 1e3) / 1e9,
+                              "frac_of_ceiling": (l2_bytes / (med_c / 1e3) / 1e9 / ceiling) if ceiling else None}}
         if key == "cfg3_f16":
             case["frame"] = _cfg3_frame(feats, dev, stream, reps, Q, P, G, C, L, cams)
         res["cases"][key] = case

@@ -71,10 +71,44 @@ def stalls(d):
     return dict(sorted(out.items(), key=lambda kv: -kv[1])[:6])
 
 
+def opcode_mix(rep: Path, top=16):
+    """Executed SASS instructions per opcode (all kernels of the capture), from the source page."""
+    out = subprocess.run(["ncu", "-i", str(rep), "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    mixes, cur = [], None
+    for row in csv.reader(out.splitlines()):
+        if len(row) >= 2 and row[0] == "Kernel Name":
+            cur = [row[1], defaultdict(int), None]
+            mixes.append(cur)
+            continue
+        if cur is None or not row:
+            continue
+        if row[0] == "Address":
+            cur[2] = (row.index("Source"), row.index("Instructions Executed"))
+            continue
+        if cur[2] is None or len(row) <= cur[2][1]:
+            continue
+        try:
+            n = int(row[cur[2][1]])
+        except ValueError:
+            continue
+        t = row[cur[2][0]].strip().split()
+        if not t:
+            continue
+        op = t[1] if t[0].startswith("@") and len(t) > 1 else t[0]
+        cur[1][op.split(".")[0]] += n
+    res = []
+    for name, mix, _ in mixes:
+        total = sum(mix.values()) or 1
+        res.append((name, total, sorted(mix.items(), key=lambda kv: -kv[1])[:top]))
+    return res
+
+
 def summarise_rep(rep: Path, dst: Path):
     lines = []
     traffic = None
-    for d in raw(rep):
+    mixes = opcode_mix(rep)  # same kernel order as the raw page
+    for i, d in enumerate(raw(rep)):
         name = d.get("Kernel Name", ("?", ""))[0]
         lines.append(f"## `{name}`\n")
         lines.append("| metric | value | unit |\n|---|---|---|")
@@ -83,6 +117,10 @@ def summarise_rep(rep: Path, dst: Path):
                 lines.append(f"| {k} | {d[k][0]} | {d[k][1]} |")
         lines.append("\nTop stall reasons (pc samples): " +
                      ", ".join(f"{k} {int(v)}" for k, v in stalls(d).items()) + "\n")
+        mix = mixes[i] if i < len(mixes) else None
+        if mix:
+            lines.append(f"Executed SASS opcodes (top of {mix[1]:,}): " +
+                         ", ".join(f"{op} {n / mix[1]:.1%}" for op, n in mix[2]) + "\n")
         if "dram__bytes_read.sum" in d:
             traffic = to_bytes(*d["dram__bytes_read.sum"]) + to_bytes(*d["dram__bytes_write.sum"])
     out = dst / (f"ncu_{rep.stem}.md")
@@ -144,6 +182,21 @@ def main():
             traffic = t
     if (src / "launches.csv").exists():
         summarise_launches(src / "launches.csv", dst)
+    for extra in sorted(src.glob("launches_*.csv")):  # other launch lists: plain per-kernel tables
+        rows = [r for r in csv.reader(l for l in extra.read_text().splitlines() if not l.startswith("=="))]
+        if not rows:
+            continue
+        ik, iv = rows[0].index("Kernel Name"), rows[0].index("Metric Value")
+        tot, cnt = defaultdict(float), defaultdict(int)
+        for r in rows[1:]:
+            tot[r[ik]] += float(r[iv].replace(",", ""))
+            cnt[r[ik]] += 1
+        total = sum(tot.values()) or 1.0
+        body = ["| kernel | launches | mean us | share |", "|---|---|---|---|"]
+        for k in sorted(tot, key=lambda k: -tot[k]):
+            body.append(f"| `{k[:90]}` | {cnt[k]} | {tot[k] / cnt[k] / 1e3:.1f} | {tot[k] / total:.1%} |")
+        (dst / f"{extra.stem}.md").write_text(f"# ncu launch list {extra.name} (gpu__time_duration.sum)\n\n" +
+                                              "\n".join(body) + "\n")
     for f in ("bench.json", "paths.jsonl"):
         if (src / f).exists():
             (dst / f).write_text((src / f).read_text())

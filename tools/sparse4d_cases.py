@@ -45,14 +45,28 @@ def make_dense_inputs(bs, Q, P, cams, L, G, dev, seed=1):
     return loc, w
 
 
-def touched_bytes(feats, loc, esize):
+def staged_fine_levels(levels, dtype):
+    """The dense FAST split the library makes (csrc/msda_staged.cu
+    dense_staged_fine_levels): 2-byte storage, 4 levels, levels 2-3 of every
+    camera fit 120 KB as 128-B row slices padded to 64-row TMA boxes -> the
+    gather moves levels 0-1 from L2, levels 2-3 come from shared memory.
+    Returns 2, or None when the anchor-major gather takes every level."""
+    if torch.finfo(dtype).bits != 16 or len(levels) != 4:
+        return None
+    stage = sum((h * w + 63) // 64 * 64 * 128 for h, w in levels[2:])
+    return 2 if stage <= 120 * 1024 else None
+
+
+def touched_bytes(feats, loc, esize, per_level=False):
     """(unique in-bounds corner cells x C x esize, every in-grid corner row the
-    gather moves L2 -> SM x C x esize) of a dense sampling."""
+    gather moves L2 -> SM x C x esize) of a dense sampling (SURVEY §8(d));
+    ``per_level`` adds the gathered bytes of each level."""
     shape = feats.spatial_shape.long()
     start = feats.scale_start_index
     bs, Q, P, cams, _ = loc.shape
     L = shape.shape[1]
     idx = []
+    lv_moved = [0] * L
     for c in range(cams):
         for m in range(L):
             H, W = int(shape[c, m, 0]), int(shape[c, m, 1])
@@ -65,17 +79,20 @@ def touched_bytes(feats, loc, esize):
                     ok = (x >= 0) & (x < W) & (y >= 0) & (y < H)
                     b = torch.arange(bs, device=loc.device).view(bs, 1, 1).expand_as(x)
                     idx.append((b * feats.table.shape[1] + int(start[c, m]) + y * W + x)[ok])
+                    lv_moved[m] += int(idx[-1].numel()) * feats.channels * esize
     rows = torch.cat(idx)
-    return torch.unique(rows).numel() * feats.channels * esize, rows.numel() * feats.channels * esize
+    res = torch.unique(rows).numel() * feats.channels * esize, rows.numel() * feats.channels * esize
+    return (*res, lv_moved) if per_level else res
 
 
 def algorithmic_bytes(feats, loc, w, esize):
     """SURVEY §8(d) dense figure: touched feature bytes + locations + weights + f32 output."""
-    tb, moved = touched_bytes(feats, loc, esize)
+    tb, moved, lv = touched_bytes(feats, loc, esize, per_level=True)
     bs, Q = loc.shape[:2]
     total = tb + loc.numel() * 4 + w.numel() * 4 + bs * Q * feats.channels * 4
     return {"touched_feature_bytes": int(tb), "input_bytes": int(loc.numel() * 4 + w.numel() * 4),
-            "output_bytes": int(bs * Q * feats.channels * 4), "total": int(total), "gathered_corner_bytes": int(moved)}
+            "output_bytes": int(bs * Q * feats.channels * 4), "total": int(total), "gathered_corner_bytes": int(moved),
+            "gathered_corner_bytes_per_level": [int(x) for x in lv]}
 
 
 def host_view(feats):
