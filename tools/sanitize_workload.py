@@ -27,7 +27,9 @@ for dt in (torch.float32, torch.float16, torch.bfloat16):
     for prec in ("fast", "fast_h2", "exact"):
         if prec == "fast_h2" and dt is not torch.float16:
             continue
-        ops.deformable_aggregation(feats, None, None, loc, w, precision=prec, normalize=True, check=True)
+        # normalize=False: the fused one-pass EXACT kernel; f16/bf16 FAST: staged coarse levels (TMA) + fine gather
+        for norm in (True, False):
+            ops.deformable_aggregation(feats, None, None, loc, w, precision=prec, normalize=norm, check=True)
     K = np.array([[300.0, 300.0, 352.0, 128.0]] * 2)
     R = np.stack([np.eye(3), np.eye(3)]).reshape(2, 9)
     T = np.array([[0.0, 0.0, 10.0], [0.0, 0.0, 12.0]])
@@ -77,5 +79,13 @@ sc = ops.PaintScene(cams, [[704, 256]] * 2, [8.0, 16.0], 32, [[0, 0, 0, 1, 1, 1,
 sc.run(seed=3)
 sc.run(background=np.zeros((sc.rows, 32)))
 ops.association_cost(np.zeros((20, 3)), np.ones((17, 3)), np.random.rand(20, 130), np.random.rand(17, 130), device=dev)
+# bilinear_sample through the host entry point (pageable grid: copied; a reused large grid: page-locked, read in place)
+from paper_2601_10819_b200 import features as F
+pyr = F.FeaturePyramid(0, [F.FeatureGrid(stride=4.0, values=np.random.rand(9, 7, 6).astype(np.float32))])
+for u, v in [(0.3, 0.2), (-1.5, 3.0), (6.0, 8.0)]:
+    F.bilinear_sample(pyr, 0, u, v)
+big = F.FeaturePyramid(0, [F.FeatureGrid(stride=4.0, values=np.random.rand(512, 1024, 4).astype(np.float32))])
+for _ in range(3):
+    F.bilinear_sample(big, 0, 100.5, 200.25)
 torch.cuda.synchronize()
 print("sanitizer workload done")
