@@ -148,17 +148,26 @@ __global__ void __launch_bounds__(32) dense_exact_kernel(const DenseExactArgs a)
           dst[1] = make_float4(pw[l][4], pw[l][5], pw[l][6], pw[l][7]);
         }
       } else {  // exact (v, u) ties: each group orders its tie set by its own weight, then position
+        uint32_t oi[kGW];
+        int sg[kGW];
 #pragma unroll
         for (int g = 0; g < kGW; ++g) {
-          const uint32_t oi = ord_f32(pw[l][g]);
-          int sg = below;
-          for (int j = 0; j < a.P; ++j) {
-            const unsigned long long kj = __shfl_sync(0xffffffffu, key, j);
-            const uint32_t oj = __shfl_sync(0xffffffffu, oi, j);
-            sg += (j != lane && kj == key && (oj < oi || (oj == oi && j < lane))) ? 1 : 0;
-          }
-          if (act) wn_w[(run0 + sg) * kGW + g] = pw[l][g];
+          oi[g] = ord_f32(pw[l][g]);
+          sg[g] = below;
         }
+#pragma unroll 1
+        for (int j = 0; j < a.P; ++j) {
+          const unsigned long long kj = __shfl_sync(0xffffffffu, key, j);
+          const bool same = j != lane && kj == key;
+#pragma unroll
+          for (int g = 0; g < kGW; ++g) {
+            const uint32_t oj = __shfl_sync(0xffffffffu, oi[g], j);
+            sg[g] += (same && (oj < oi[g] || (oj == oi[g] && j < lane))) ? 1 : 0;
+          }
+        }
+        if (act)
+#pragma unroll
+          for (int g = 0; g < kGW; ++g) wn_w[(run0 + sg[g]) * kGW + g] = pw[l][g];
       }
     }
     __syncwarp();
