@@ -77,7 +77,7 @@ __device__ __forceinline__ float lds32f(uint32_t addr) {
 template <typename T, int VEC, int D>
 __global__ void __launch_bounds__(32) dense_exact_kernel(const DenseExactArgs a) {
   constexpr int BYTES = VEC * (int)sizeof(T);
-  static_assert(BYTES == 16, "16-B lanes");
+  static_assert(BYTES == 16 || BYTES == 8, "8- or 16-B lanes");  // (8-B lanes, two warps per query: 1268 vs 957 us at cfg3)
   using SM = DxSmem<BYTES, D>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int NB = a.ncs_pad;  // samples per camera buffer
@@ -203,8 +203,15 @@ __global__ void __launch_bounds__(32) dense_exact_kernel(const DenseExactArgs a)
     float c[4][VEC];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint4 cv = lds128(ring + slot * SM::kSlot + k * 32 * BYTES);
-      to_f32<T, VEC>(*reinterpret_cast<const RawVec<BYTES>*>(&cv), c[k]);
+      RawVec<BYTES> cv;
+      if constexpr (BYTES == 16) {
+        cv.v = lds128(ring + slot * SM::kSlot + k * 32 * BYTES);
+      } else {
+        asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];"
+                     : "=r"(cv.v.x), "=r"(cv.v.y)
+                     : "r"(ring + slot * SM::kSlot + k * 32 * BYTES));
+      }
+      to_f32<T, VEC>(cv, c[k]);
     }
     const float2 w0 = make_float2(__uint_as_float(iwr.x), __uint_as_float(iwr.x));
     const float2 w1 = make_float2(__uint_as_float(iwr.y), __uint_as_float(iwr.y));
@@ -246,6 +253,24 @@ __global__ void __launch_bounds__(32) dense_exact_kernel(const DenseExactArgs a)
       cp_async_commit();
     };
     int j = 0;
+    if constexpr (D >= 8) {  // four samples per step: their trees overlap, the adds stay in order
+      for (; j + 3 < n_cs; j += 4, g += 4) {
+        cp_async_wait<D - 4>();
+        float t0[VEC], t1[VEC], t2[VEC], t3[VEC];
+        tree(buf + j, g % D, t0);
+        tree(buf + j + 1, (g + 1) % D, t1);
+        tree(buf + j + 2, (g + 2) % D, t2);
+        tree(buf + j + 3, (g + 3) % D, t3);
+        add(t0);
+        add(t1);
+        add(t2);
+        add(t3);
+        refill(j, g % D);
+        refill(j + 1, (g + 1) % D);
+        refill(j + 2, (g + 2) % D);
+        refill(j + 3, (g + 3) % D);
+      }
+    }
     for (; j + 1 < n_cs; j += 2, g += 2) {  // two samples: their trees overlap, the adds stay in order
       cp_async_wait<D - 2>();
       float t0[VEC], t1[VEC];
