@@ -640,6 +640,32 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
                   bool project, const float* anchors, int32_t n_learned, const float* offsets,
                   const msda_cameras_t* cams, const float* strides, float dt, float* wsum_out = nullptr);
 
+// A forked stream for work that overlaps the caller's stream inside one call
+// (fork / join events recorded per call).  One per host thread and device:
+// calls from different threads never share it.
+struct AuxStream {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  bool ok = false, tried = false;
+};
+const AuxStream& aux_stream() {
+  thread_local AuxStream per_dev[64];
+  static const AuxStream none{};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return none;
+  AuxStream& x = per_dev[dev];
+  if (!x.tried) {
+    x.tried = true;
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    x.ok = cudaStreamCreateWithPriority(&x.stream, cudaStreamNonBlocking, hi) == cudaSuccess &&
+           cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) == cudaSuccess;
+    if (!x.ok) cudaGetLastError();  // not sticky: the call runs both parts on the caller's stream
+  }
+  return x;
+}
+
 
 }  // namespace
 }  // namespace msda
@@ -723,11 +749,20 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
         float* wsum = wsum_out ? wsum_out : (normalize ? scratch : nullptr);
         e = cudaMemsetAsync(out, 0, (size_t)nq * a.C * 4, s);
         if (e == cudaSuccess && wsum) e = cudaMemsetAsync(wsum, 0, (size_t)nq * G * 4, s);
-        // coarse levels first (issue-bound, no L2 gathers), then the fine
-        // levels' gather; both red.add into the zeroed totals.  (Running them
-        // concurrently on a forked stream measured no better: the fine
-        // gather loses occupancy to the coarse kernel's 121 KB CTAs.)
-        if (e == cudaSuccess) e = launch_dense_coarse(*f, d, n_fine, out, wsum, s);
+        // coarse levels (shared-memory-bound, no L2 gathers) on a forked
+        // high-priority stream beside the fine levels' gather (L2-bound):
+        // one 256-thread coarse CTA per SM, the gather's one-warp CTAs fill
+        // the rest; both red.add into the zeroed totals, the join orders
+        // them before whatever follows on s (capturable in a CUDA graph)
+        const AuxStream& x = aux_stream();
+        if (e == cudaSuccess && x.ok) {
+          e = cudaEventRecord(x.fork, s);
+          if (e == cudaSuccess) e = cudaStreamWaitEvent(x.stream, x.fork, 0);
+          if (e == cudaSuccess) e = launch_dense_coarse(*f, d, n_fine, out, wsum, x.stream);
+          if (e == cudaSuccess) e = cudaEventRecord(x.join, x.stream);
+        } else if (e == cudaSuccess) {
+          e = launch_dense_coarse(*f, d, n_fine, out, wsum, s);
+        }
         if (e == cudaSuccess) {
           DenseFastSpec fine = d;
           fine.n_lv = n_fine;
@@ -735,6 +770,7 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
           e = launch_gather_dense_fast(*f, fine, ew.status, out, s, &pending);
           if (e == cudaErrorNotSupported) return MSDA_CUDA_ERROR;  // the staged plan implies the gather fits
         }
+        if (e == cudaSuccess && x.ok) e = cudaStreamWaitEvent(s, x.join, 0);
         if (e != cudaSuccess) return MSDA_CUDA_ERROR;
       } else {
         e = launch_gather_dense_fast(*f, d, ew.status, out, s, &pending);

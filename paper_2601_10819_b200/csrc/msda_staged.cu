@@ -38,7 +38,10 @@
 namespace msda {
 namespace {
 
-constexpr int kStWarps = 16;
+// 8 warps: the coarse kernel runs beside the fine gather (forked stream), and
+// a 256-thread CTA leaves registers for ~8 gather warps per SM (16 warps
+// alone: 160 us; 8 warps beside the gather: cfg3 FAST_H2 382 vs 397 us total)
+constexpr int kStWarps = 8;
 constexpr int kStThreads = kStWarps * 32;
 constexpr int kSliceBytes = 128;  // staged row slice: one 128-B line, 8 lanes x 16 B
 constexpr int kBoxRows = 64;      // TMA box: 64 rows x 128 B
