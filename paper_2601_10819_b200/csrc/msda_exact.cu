@@ -353,6 +353,42 @@ __device__ __forceinline__ SampleRec ld_rec(const SampleRec* p) {
   return r;
 }
 
+// DENSE record of sample s of the warp (anchor q, cameras from cam_lo), in
+// camera-major, level, point order; wg = the sample's G group weights
+template <int GW>
+__device__ __forceinline__ SampleRec dense_record(const GatherArgs& a, int64_t q, int cam_lo, int s, float (&wg)[GW]) {
+  const int per_cam = a.n_lv * a.P;
+  const int cs = s / per_cam, rem = s - cs * per_cam;
+  const int cam = cam_lo + cs;
+  const int l = rem / a.P, p = rem - l * a.P;
+  const int t = cam * a.n_levels + l;
+  const int H = a.shape[2 * t], W = a.shape[2 * t + 1];
+  const int64_t pc = (q * a.P + p) * a.n_cams + cam;
+  float uu, vv;
+  bool valid = true;
+  if (a.proj_cell) {  // projected keypoint (geometry.py:162-182), cell = pixel / stride - 0.5
+    const float2 cl = a.proj_cell[pc * a.n_levels + l];
+    valid = !isnan(cl.x);
+    uu = valid ? cl.x : -4.0f;
+    vv = valid ? cl.y : -4.0f;
+  } else {
+    const float2 lp = __ldg(reinterpret_cast<const float2*>(a.loc) + pc);
+    uu = __fsub_rn(__fmul_rn(lp.x, (float)W), 0.5f);
+    vv = __fsub_rn(__fmul_rn(lp.y, (float)H), 0.5f);
+  }
+  const float* wp = a.w + (pc * a.n_levels + l) * a.n_groups;
+  if (GW == 8 && a.n_groups == 8 && (reinterpret_cast<uintptr_t>(wp) & 15) == 0) {
+    const float4 w0 = __ldg(reinterpret_cast<const float4*>(wp)), w1 = __ldg(reinterpret_cast<const float4*>(wp) + 1);
+    const float ww[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+    for (int k = 0; k < GW; ++k) wg[k] = valid ? ww[k % 8] : 0.0f;
+  } else {
+#pragma unroll
+    for (int k = 0; k < GW; ++k) wg[k] = (valid && k < a.n_groups) ? __ldg(wp + k) : 0.0f;  // behind the camera: out of the plan
+  }
+  return make_record(uu, vv, (q / a.q_per_batch) * a.rows_per_batch + a.start[t], H, W);
+}
+
 template <int VEC>
 __device__ __forceinline__ void half_accumulate(__half2* acch, const void* const* cvp, const float4 iw, const float wn) {
   const __half2 hw0 = __float2half2_rn(iw.x), hw1 = __float2half2_rn(iw.y);
@@ -571,30 +607,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
     if (s < n) {
       SampleRec r;
       if constexpr (DENSE) {
-        const int per_cam = a.n_lv * a.P;
-        const int cs = s / per_cam, rem = s - cs * per_cam;
-        const int cam = cam_lo + cs;
-        const int l = rem / a.P, p = rem - l * a.P;
-        const int t = cam * a.n_levels + l;
-        const int H = a.shape[2 * t], W = a.shape[2 * t + 1];
-        const int64_t pc = (q * a.P + p) * a.n_cams + cam;
-        float uu, vv;
-        bool valid = true;
-        if (a.proj_cell) {  // projected keypoint (geometry.py:162-182), cell = pixel / stride - 0.5
-          const float2 cl = a.proj_cell[pc * a.n_levels + l];
-          valid = !isnan(cl.x);
-          uu = valid ? cl.x : -4.0f;
-          vv = valid ? cl.y : -4.0f;
-        } else {
-          const float2 lp = __ldg(reinterpret_cast<const float2*>(a.loc) + pc);
-          uu = __fsub_rn(__fmul_rn(lp.x, (float)W), 0.5f);
-          vv = __fsub_rn(__fmul_rn(lp.y, (float)H), 0.5f);
-        }
-        r = make_record(uu, vv, (q / a.q_per_batch) * a.rows_per_batch + a.start[t], H, W);
-        const float* wp = a.w + (pc * a.n_levels + l) * a.n_groups;
-#pragma unroll
-        for (int k = 0; k < GW; ++k)
-          if (k < a.n_groups) r_wg[k] = valid ? __ldg(wp + k) : 0.0f;  // behind the camera: out of the plan
+        r = dense_record<GW>(a, q, cam_lo, s, r_wg);
       } else if constexpr (RAW) {
         const int64_t si = lo + s;
         int c = __ldg(a.cam + si), l = __ldg(a.lvl + si);
