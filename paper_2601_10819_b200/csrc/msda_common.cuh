@@ -247,7 +247,7 @@ __device__ __forceinline__ void cp_async_zfill(uint32_t dst, const void* src, bo
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N));
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 // ---- the reference's exact f32 expression tree ----

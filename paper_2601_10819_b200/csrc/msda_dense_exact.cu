@@ -68,11 +68,6 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
   return v;
 }
-__device__ __forceinline__ float lds32f(uint32_t addr) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-  return v;
-}
 
 template <typename T, int VEC, int D>
 __global__ void __launch_bounds__(32) dense_exact_kernel(const DenseExactArgs a) {
@@ -84,9 +79,8 @@ __global__ void __launch_bounds__(32) dense_exact_kernel(const DenseExactArgs a)
   const int lane = threadIdx.x;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_raw);
   const uint32_t ring = sbase + lane * BYTES;           // + slot * kSlot + corner * 32 * BYTES
+  const unsigned char* ring_ptr = smem_raw + lane * BYTES;
   const uint32_t s_rows = sbase + SM::kRing;            // int4 [2][NB]
-  const uint32_t s_iw = s_rows + 2 * NB * 16;           // float4 [2][NB]
-  const uint32_t s_wn = s_iw + 2 * NB * 16;             // float [2][NB][kGW]
   int4* rows_w = reinterpret_cast<int4*>(smem_raw + SM::kRing);
   float4* iw_w = reinterpret_cast<float4*>(smem_raw + SM::kRing + 2 * NB * 16);
   float* wn_w = reinterpret_cast<float*>(smem_raw + SM::kRing + 4 * NB * 16);
@@ -198,14 +192,14 @@ __global__ void __launch_bounds__(32) dense_exact_kernel(const DenseExactArgs a)
   uint32_t g = 0;  // global sample index; ring slot = g % D
   // one sample: its exact tree (products, sums, weight) — independent of acc
   auto tree = [&](int idx, uint32_t slot, float (&tw)[VEC]) {
-    const uint4 iwr = lds128(s_iw + idx * 16);
-    const float wn = lds32f(s_wn + (idx * kGW + gl) * 4);
+    const uint4 iwr = *reinterpret_cast<const uint4*>(iw_w + idx);
+    const float wn = wn_w[idx * kGW + gl];
     float c[4][VEC];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       RawVec<BYTES> cv;
       if constexpr (BYTES == 16) {
-        cv.v = lds128(ring + slot * SM::kSlot + k * 32 * BYTES);
+        cv.v = *reinterpret_cast<const uint4*>(ring_ptr + slot * SM::kSlot + k * 32 * BYTES);
       } else {
         asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];"
                      : "=r"(cv.v.x), "=r"(cv.v.y)
