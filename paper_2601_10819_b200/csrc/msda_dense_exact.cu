@@ -69,6 +69,62 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   return v;
 }
 
+// Canonicalise the keypoint run (camera cam, level l) of a query: lane p < P
+// holds keypoint p's location lp and group weights pwl; each record goes to
+// its canonical slot run0 + rank (features.py:261-263).  Exact (v, u) ties —
+// identical records — are ordered per group by that group's weight, then
+// position (the lexsort's last keys).
+__device__ __forceinline__ void stage_run(const DenseExactArgs& a, int lane, bool act, float2 lp,
+                                          const float (&pwl)[kGW], int cam, int l, int64_t row_base, int run0,
+                                          int4* rows_w, float4* iw_w, float* wn_w) {
+  const int t = cam * a.L + l;
+  const int H = a.shape[2 * t], W = a.shape[2 * t + 1];
+  const float u = __fsub_rn(__fmul_rn(lp.x, (float)W), 0.5f);  // cell = loc * W - 0.5 (features.py:20-24)
+  const float v = __fsub_rn(__fmul_rn(lp.y, (float)H), 0.5f);
+  const unsigned long long key = ((unsigned long long)ord_f32(v) << 32) | ord_f32(u);
+  int below = 0, eq_before = 0;
+  bool tie = false;
+  for (int j = 0; j < a.P; ++j) {
+    const unsigned long long kj = __shfl_sync(0xffffffffu, key, j);
+    below += kj < key ? 1 : 0;
+    tie |= (kj == key) & (j != lane);
+    eq_before += (kj == key) & (j < lane) ? 1 : 0;
+  }
+  const SampleRec r = make_record(u, v, row_base + a.start[t], H, W);
+  if (act) {  // tied records are identical: any slot of the tie set holds the same record
+    rows_w[run0 + below + eq_before] = make_int4(r.row[0], r.row[1], r.row[2], r.row[3]);
+    iw_w[run0 + below + eq_before] = make_float4(r.iw[0], r.iw[1], r.iw[2], r.iw[3]);
+  }
+  if (!__any_sync(0xffffffffu, act && tie)) {
+    if (act) {
+      float4* dst = reinterpret_cast<float4*>(wn_w + (run0 + below) * kGW);
+      dst[0] = make_float4(pwl[0], pwl[1], pwl[2], pwl[3]);
+      dst[1] = make_float4(pwl[4], pwl[5], pwl[6], pwl[7]);
+    }
+  } else {
+    uint32_t oi[kGW];
+    int sg[kGW];
+#pragma unroll
+    for (int g = 0; g < kGW; ++g) {
+      oi[g] = ord_f32(pwl[g]);
+      sg[g] = below;
+    }
+#pragma unroll 1
+    for (int j = 0; j < a.P; ++j) {
+      const unsigned long long kj = __shfl_sync(0xffffffffu, key, j);
+      const bool same = j != lane && kj == key;
+#pragma unroll
+      for (int g = 0; g < kGW; ++g) {
+        const uint32_t oj = __shfl_sync(0xffffffffu, oi[g], j);
+        sg[g] += (same && (oj < oi[g] || (oj == oi[g] && j < lane))) ? 1 : 0;
+      }
+    }
+    if (act)
+#pragma unroll
+      for (int g = 0; g < kGW; ++g) wn_w[(run0 + sg[g]) * kGW + g] = pwl[g];
+  }
+}
+
 template <typename T, int VEC, int D>
 __global__ void __launch_bounds__(32) dense_exact_kernel(const DenseExactArgs a) {
   constexpr int BYTES = VEC * (int)sizeof(T);
@@ -112,57 +168,10 @@ __global__ void __launch_bounds__(32) dense_exact_kernel(const DenseExactArgs a)
   };
   // stage camera `cam`'s runs in canonical order into buffer `buf` from the prefetched inputs
   auto stage_camera = [&](int cam, int buf) {
-    const float2 lp = pl;
 #pragma unroll
     for (int l = 0; l < kMaxLv; ++l) {
       if (l >= a.L) break;
-      const int t = cam * a.L + l;
-      const int H = a.shape[2 * t], W = a.shape[2 * t + 1];
-      const float u = __fsub_rn(__fmul_rn(lp.x, (float)W), 0.5f);  // cell = loc * W - 0.5 (features.py:20-24)
-      const float v = __fsub_rn(__fmul_rn(lp.y, (float)H), 0.5f);
-      const unsigned long long key = ((unsigned long long)ord_f32(v) << 32) | ord_f32(u);
-      int below = 0, eq_before = 0;
-      bool tie = false;
-      for (int j = 0; j < a.P; ++j) {
-        const unsigned long long kj = __shfl_sync(0xffffffffu, key, j);
-        below += kj < key ? 1 : 0;
-        tie |= (kj == key) & (j != lane);
-        eq_before += (kj == key) & (j < lane) ? 1 : 0;
-      }
-      const SampleRec r = make_record(u, v, row_base + a.start[t], H, W);
-      const int run0 = buf * NB + l * a.P;
-      if (act) {  // tied records are identical: any slot of the tie set holds the same record
-        rows_w[run0 + below + eq_before] = make_int4(r.row[0], r.row[1], r.row[2], r.row[3]);
-        iw_w[run0 + below + eq_before] = make_float4(r.iw[0], r.iw[1], r.iw[2], r.iw[3]);
-      }
-      if (!__any_sync(0xffffffffu, act && tie)) {
-        if (act) {
-          float4* dst = reinterpret_cast<float4*>(wn_w + (run0 + below) * kGW);
-          dst[0] = make_float4(pw[l][0], pw[l][1], pw[l][2], pw[l][3]);
-          dst[1] = make_float4(pw[l][4], pw[l][5], pw[l][6], pw[l][7]);
-        }
-      } else {  // exact (v, u) ties: each group orders its tie set by its own weight, then position
-        uint32_t oi[kGW];
-        int sg[kGW];
-#pragma unroll
-        for (int g = 0; g < kGW; ++g) {
-          oi[g] = ord_f32(pw[l][g]);
-          sg[g] = below;
-        }
-#pragma unroll 1
-        for (int j = 0; j < a.P; ++j) {
-          const unsigned long long kj = __shfl_sync(0xffffffffu, key, j);
-          const bool same = j != lane && kj == key;
-#pragma unroll
-          for (int g = 0; g < kGW; ++g) {
-            const uint32_t oj = __shfl_sync(0xffffffffu, oi[g], j);
-            sg[g] += (same && (oj < oi[g] || (oj == oi[g] && j < lane))) ? 1 : 0;
-          }
-        }
-        if (act)
-#pragma unroll
-          for (int g = 0; g < kGW; ++g) wn_w[(run0 + sg[g]) * kGW + g] = pw[l][g];
-      }
+      stage_run(a, lane, act, pl, pw[l], cam, l, row_base, buf * NB + l * a.P, rows_w, iw_w, wn_w);
     }
     __syncwarp();
   };
