@@ -702,6 +702,8 @@ def sparse4d_block(args, dev, smi_index):
                               "frac_of_ceiling": (l2_bytes / (med_c / 1e3) / 1e9 / ceiling) if ceiling else None}}
         if key == "cfg3_f16":
             case["frame"] = _cfg3_frame(feats, dev, stream, reps, Q, P, G, C, L, cams)
+        if key == "cfg4_bf16":
+            case["full_path"] = _cfg4_full_path(feats, loc, w, out, dev, stream, flush_buf, reps, cams, Q, C)
         res["cases"][key] = case
         del feats, loc, w, out, ref
         torch.cuda.empty_cache()
@@ -747,6 +749,66 @@ def _project_case(dev, stream, flush_buf, reps, peak, cams=6, Q=900, C=256, G=8,
             "path": "msda_dense_project: projection pre-pass + pipelined gather",
             "latency_us": cold[len(cold) // 2] * 1e3, "warm_us": warm[len(warm) // 2] * 1e3,
             "max_rel_err_vs_oracle_24_anchors": err, "tolerance": 1e-4, "within_tolerance": err <= 1e-4}
+
+
+def _cfg4_full_path(feats, loc, w, out, dev, stream, flush_buf, reps, cams, Q, C):
+    """BASELINE configs[3]: the full aggregation path at 32 bf16 cameras —
+    deformable_aggregation (FAST) over the feature table, then occlusion-aware
+    ReID pooling on the same table (oae_pool: keypoints and f64 projection,
+    level-mean f32 bilinear reads, softmax(desc . g / sqrt(D)), visibility-
+    weighted fusion, L2 normalisation / memory fallback; oae.py:81-164).  OAE
+    parity on 8 queries against the oracle (oae.py restated, f64) on the
+    features the GPU reads, 1e-4 on the unit embedding; then cold / warm
+    timing of the pooling alone and of the chained path."""
+    import torch
+
+    from oracle import msda_oracle as mo
+    from paper_2601_10819_b200 import ops
+    from tools import sparse4d_cases as s4
+
+    K, R, T = s4.ring(cams)
+    camd = ops.Cameras(K, R, T, device=dev)
+    anchors = s4.anchors_for(Q, dev)
+    offs = (torch.rand((6, 3), generator=torch.Generator().manual_seed(3)) * 2 - 1).to(dev)
+    strides = [4.0, 8.0, 16.0, 32.0]
+    strides_d = torch.tensor(strides, device=dev)
+    g = torch.Generator(device=dev).manual_seed(4)
+    desc = torch.randn((Q, C), generator=g, device=dev)
+    vis = torch.rand((Q, cams), generator=g, device=dev)
+    mem = torch.nn.functional.normalize(torch.randn((Q, C), generator=g, device=dev), dim=1)
+    emb, occl = ops.oae_pool(feats, anchors, offs, camd, strides_d, desc, vis, mem, check=True)
+    table, tiles, _ = s4.host_view(feats)
+    nq, err, occ_ok = 8, 0.0, True
+    an, of = anchors.cpu().double().numpy(), offs.cpu().double().numpy()
+    de, vi, me = desc.cpu().double().numpy(), vis.cpu().numpy(), mem.cpu().double().numpy()
+    e_host, o_host = emb[:nq].cpu().numpy(), occl[:nq].cpu().numpy()
+    for q in range(nq):
+        kps = mo.keypoints(an[q], of)
+        views = [mo.extract_view(table, tiles, 4, c, strides, K[c], R[c], T[c], kps, de[q]) for c in range(cams)]
+        ref, ref_occ = mo.fuse(views, vi[q], me[q])
+        err = max(err, float(np.abs(e_host[q] - ref).max()))
+        occ_ok &= bool(o_host[q]) == ref_occ
+    del table
+    pool = lambda: ops.oae_pool(feats, anchors, offs, camd, strides_d, desc, vis, mem, check=False)  # noqa: E731
+
+    def full():
+        ops.deformable_aggregation(feats, None, None, loc, w, precision="fast", out=out)
+        pool()
+
+    res = {"desc": "MSDA (deformable_aggregation FAST, 900 anchors x 13 pts x 32 cams x 4 levels, G=8) then OAE "
+                   "ReID pooling (900 queries: 7 fixed + 6 learned keypoints projected through 32 ring cameras, "
+                   "4 levels, softmax over keypoints, visibility-weighted fusion) on the same bf16 table",
+           "oae_max_abs_err_vs_oracle_8_queries": err, "oae_tolerance": 1e-4, "oae_occluded_flags_equal": occ_ok,
+           "within_tolerance": bool(err <= 1e-4 and occ_ok)}
+    for name, fn in (("oae_pool", pool), ("msda_then_oae", full)):
+        for _ in range(3):
+            fn()
+        cold = _time_events(fn, reps, stream, flush_buf)
+        warm = _time_events(fn, reps, stream)
+        res[name] = {"latency_us": cold[len(cold) // 2] * 1e3, "warm_us": warm[len(warm) // 2] * 1e3,
+                     "queries_per_s": Q / (cold[len(cold) // 2] / 1e3),
+                     "camera_frames_per_s": cams / (cold[len(cold) // 2] / 1e3)}
+    return res
 
 
 def _cfg3_frame(feats, dev, stream, reps, Q, P, G, C, L, cams, layers=6):
