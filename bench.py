@@ -656,14 +656,18 @@ def sparse4d_block(args, dev, smi_index):
         # ---- parity against the C oracle on the features the GPU reads ----
         t0 = time.time()
         table, tiles, shape = s4.host_view(feats)
-        ref = ob.msda_dense_groups_c(table, tiles, shape, loc.cpu().numpy(), w.cpu().numpy(), L, normalize=False)
-        del table
+        loc_h, w_h = loc.cpu().numpy(), w.cpu().numpy()
+        ref = ob.msda_dense_groups_c(table, tiles, shape, loc_h, w_h, L, normalize=False)
         oracle_s = time.time() - t0
+        cpu_ref = None if getattr(args, "no_cpu", False) else _cpu_ref_dense(table, tiles, shape, loc_h, w_h, ref)
+        del table
         scale = float(np.abs(ref).max())
         case = {"desc": desc, "cams": cams, "dtype": dt_name, "queries": Q, "points": P, "groups": G, "channels": C,
                 "levels": [list(x) for x in levels], "algorithmic_bytes": ab,
                 "l2": "flushed per call" if feats.table.numel() * esize < 2 * L2_BYTES else "table larger than L2",
                 "oracle_s": oracle_s, "paths": {}}
+        if cpu_ref is not None:
+            case["cpu_reference"] = cpu_ref
         n_fine = s4.staged_fine_levels(levels, dtype)
         for prec in precs:
             fn = (lambda p=prec: ops.deformable_aggregation(feats, None, None, loc, w, precision=p, out=out))  # noqa
@@ -690,6 +694,7 @@ def sparse4d_block(args, dev, smi_index):
             achieved = ab["total"] / (med_c / 1e3) / 1e9
             case["paths"][prec] = {
                 **parity, "latency_us": med_c * 1e3, "best_us": cold[0] * 1e3, "warm_us": med_w * 1e3,
+                "vs_cpu_reference": (cpu_ref["full_call_s"] / (med_c / 1e3)) if cpu_ref else None,
                 "camera_frames_per_s": cams / (med_c / 1e3),
                 "streams_at_30fps_6layers": int(cams / (30 * 6 * med_c / 1e3)),
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -703,7 +708,8 @@ def sparse4d_block(args, dev, smi_index):
         if key == "cfg3_f16":
             case["frame"] = _cfg3_frame(feats, dev, stream, reps, Q, P, G, C, L, cams)
         if key == "cfg4_bf16":
-            case["full_path"] = _cfg4_full_path(feats, loc, w, out, dev, stream, flush_buf, reps, cams, Q, C)
+            case["full_path"] = _cfg4_full_path(feats, loc, w, out, dev, stream, flush_buf, reps, cams, Q, C,
+                                                cpu=not getattr(args, "no_cpu", False))
         res["cases"][key] = case
         del feats, loc, w, out, ref
         torch.cuda.empty_cache()
@@ -751,7 +757,100 @@ def _project_case(dev, stream, flush_buf, reps, peak, cams=6, Q=900, C=256, G=8,
             "max_rel_err_vs_oracle_24_anchors": err, "tolerance": 1e-4, "within_tolerance": err <= 1e-4}
 
 
-def _cfg4_full_path(feats, loc, w, out, dev, stream, flush_buf, reps, cams, Q, C):
+def _cpu_ref_dense(table, tiles, shape, loc, w, oracle_out):
+    """The reference CPU path for deformable_aggregation on this box (SURVEY
+    8(c)/(d)): per channel group g, the UNMODIFIED mvtrack3d
+    msda_optimized(FULL, normalize=False, all host threads) from
+    baseline/_ref on the pyramids sliced to g's channels and the CSR plan of
+    every (anchor, keypoint, camera, level) sample — cell = f32(f32(loc * W)
+    - 0.5), weight w[..., g] — the composition the oracle restates.  One
+    timed full call after a warm-up that builds the reference's packed-grid
+    caches; its output is compared with the oracle's bytes, i.e. with the GPU
+    EXACT path."""
+    rf = reference_features()
+    if rf is None:
+        return None
+    workers = os.cpu_count() or 1
+    _, Q, P, cams, _ = loc.shape
+    L, G, C = shape.shape[1], w.shape[-1], table.shape[1]
+    cpg = C // G
+    pyrs = [[rf.FeaturePyramid(c, [rf.FeatureGrid(stride=float(4 << m), values=np.ascontiguousarray(
+        table[st:st + H * W, g * cpg:(g + 1) * cpg]).reshape(H, W, cpg))
+        for m, (st, H, W) in enumerate(tiles[c * L:(c + 1) * L])]) for c in range(cams)] for g in range(G)]
+    Hs, Ws = shape[:, :, 0].astype(np.float32), shape[:, :, 1].astype(np.float32)  # [cams, L]
+    half = np.float32(0.5)
+
+    def plans(nq):
+        lx = loc[0, :nq, :, :, 0].astype(np.float32)[..., None]  # [nq, P, cams, 1]
+        ly = loc[0, :nq, :, :, 1].astype(np.float32)[..., None]
+        u = (lx * Ws[None, None]).astype(np.float32) - half  # features.py:20-24, two f32 roundings
+        v = (ly * Hs[None, None]).astype(np.float32) - half
+        cam_i = np.broadcast_to(np.arange(cams, dtype=np.int32)[None, None, :, None], u.shape)
+        lvl_i = np.broadcast_to(np.arange(L, dtype=np.int32)[None, None, None, :], u.shape)
+        offsets = np.arange(nq + 1, dtype=np.int64) * (P * cams * L)
+        out = []
+        for g in range(G):
+            plan = rf.SamplePlan.__new__(rf.SamplePlan)
+            plan._finalize(offsets, np.ascontiguousarray(cam_i).ravel(), np.ascontiguousarray(lvl_i).ravel(),
+                           u.ravel(), v.ravel(), np.ascontiguousarray(w[0, :nq, ..., g], dtype=np.float32).ravel())
+            out.append(plan)
+        return out
+
+    def run(nq):
+        pl = plans(nq)
+        t0 = time.perf_counter()
+        res = [rf.msda_optimized(pyrs[g], pl[g], rf.PrecisionMode.FULL, normalize=False, workers=workers)[0]
+               for g in range(G)]
+        return time.perf_counter() - t0, np.concatenate(res, axis=1)
+
+    run(max(2 * workers, Q // 50))  # warm-up: the reference's packed-pair caches of every grid
+    t, got = run(Q)  # the full call (a query subset would over-state it: the per-tile costs dominate small subsets)
+    return {"full_call_s": t, "camera_frames_per_s": cams / t, "cores": workers, "kind": "reference",
+            "sample": f"the full call: {Q} anchors x {G} channel-group calls, 1 rep after a warm-up",
+            "algorithm": f"mvtrack3d.features.msda_optimized(FULL, normalize=False, workers={workers}) per group "
+                         "from baseline/_ref",
+            "bitwise_equal_to_oracle": bool(got.tobytes() == oracle_out[0].tobytes())}
+
+
+def _cpu_ref_oae(table, tiles, K, R, T, strides, anchors, offs, desc, vis, mem, emb, nq=16):
+    """The reference's own occlusion-aware pooling on this host: for nq
+    queries, generate_keypoints -> extract_view_feature on each of the 32
+    cameras -> fuse_or_memory (oae.py:81-164; single-threaded Python as in
+    the reference), extrapolated to all queries; its embeddings are compared
+    with the GPU's."""
+    ref = ROOT / "baseline" / "_ref"
+    if reference_features() is None:
+        return None
+    from mvtrack3d import features as rf
+    from mvtrack3d import geometry as rg
+    from mvtrack3d import oae as ro
+
+    cams = K.shape[0]
+    L = len(strides)
+    pyrs = [rf.FeaturePyramid(c, [rf.FeatureGrid(stride=float(s), values=table[st:st + H * W].reshape(H, W, -1))
+                                  for s, (st, H, W) in zip(strides, tiles[c * L:(c + 1) * L])]) for c in range(cams)]
+    cm = [rg.CameraModel(float(K[c, 0]), float(K[c, 1]), float(K[c, 2]), float(K[c, 3]), R[c], T[c], 704, 256)
+          for c in range(cams)]
+    err = 0.0
+    t0 = time.perf_counter()
+    for q in range(nq):
+        st = rg.ObjectState3D(*(float(x) for x in anchors[q]))
+        kp = rg.generate_keypoints(st, offs)
+        memory = ro.Embedding.normalize(mem[q])
+        query = ro.Query(track_id=q, anchor=st, memory=memory, descriptor=desc[q])
+        pv = [ro.extract_view_feature(pyrs[c], cm[c], kp, query) for c in range(cams)]
+        e = ro.fuse_or_memory(pv, list(vis[q]), memory)
+        err = max(err, float(np.abs(e.values - emb[q]).max()))
+    t = time.perf_counter() - t0
+    Q = anchors.shape[0]
+    return {"full_call_s": t * Q / nq, "queries_per_s": nq / t, "cores": 1, "kind": "reference",
+            "sample": f"{nq} of {Q} queries x {cams} cameras, extrapolated linearly",
+            "algorithm": "mvtrack3d.oae generate_keypoints + extract_view_feature + fuse_or_memory from "
+                         f"{ref.relative_to(ROOT)}",
+            "gpu_max_abs_err_on_sample": err}
+
+
+def _cfg4_full_path(feats, loc, w, out, dev, stream, flush_buf, reps, cams, Q, C, cpu=True):
     """BASELINE configs[3]: the full aggregation path at 32 bf16 cameras —
     deformable_aggregation (FAST) over the feature table, then occlusion-aware
     ReID pooling on the same table (oae_pool: keypoints and f64 projection,
@@ -788,6 +887,7 @@ def _cfg4_full_path(feats, loc, w, out, dev, stream, flush_buf, reps, cams, Q, C
         ref, ref_occ = mo.fuse(views, vi[q], me[q])
         err = max(err, float(np.abs(e_host[q] - ref).max()))
         occ_ok &= bool(o_host[q]) == ref_occ
+    cpu = _cpu_ref_oae(table, tiles, K, R, T, strides, an, of, de, vi, me, emb.cpu().numpy()) if cpu else None
     del table
     pool = lambda: ops.oae_pool(feats, anchors, offs, camd, strides_d, desc, vis, mem, check=False)  # noqa: E731
 
@@ -800,12 +900,16 @@ def _cfg4_full_path(feats, loc, w, out, dev, stream, flush_buf, reps, cams, Q, C
                    "4 levels, softmax over keypoints, visibility-weighted fusion) on the same bf16 table",
            "oae_max_abs_err_vs_oracle_8_queries": err, "oae_tolerance": 1e-4, "oae_occluded_flags_equal": occ_ok,
            "within_tolerance": bool(err <= 1e-4 and occ_ok)}
+    if cpu is not None:
+        res["cpu_reference_oae"] = cpu
     for name, fn in (("oae_pool", pool), ("msda_then_oae", full)):
         for _ in range(3):
             fn()
         cold = _time_events(fn, reps, stream, flush_buf)
         warm = _time_events(fn, reps, stream)
         res[name] = {"latency_us": cold[len(cold) // 2] * 1e3, "warm_us": warm[len(warm) // 2] * 1e3,
+                     "vs_cpu_reference": (cpu["full_call_s"] / (cold[len(cold) // 2] / 1e3))
+                     if (cpu and name == "oae_pool") else None,
                      "queries_per_s": Q / (cold[len(cold) // 2] / 1e3),
                      "camera_frames_per_s": cams / (cold[len(cold) // 2] / 1e3)}
     return res

@@ -42,11 +42,18 @@ def main():
             print(f"{key:16s} {p:8s} {v['latency_us']:8.1f} us cold {v['warm_us']:8.1f} warm  "
                   f"hbm {v['roofline']['frac']:.3f}  l2 {v['l2_gather']['frac_of_ceiling'] or 0:.2f}  {par} "
                   f"{'OK' if ok else 'FAIL'}")
+        if "cpu_reference" in c:
+            cr = c["cpu_reference"]
+            print(f"{key:16s} cpu reference {cr['full_call_s'] * 1e3:.0f} ms ({cr['cores']} cores), bitwise "
+                  f"{cr['bitwise_equal_to_oracle']}")
         if "full_path" in c:
             fp = c["full_path"]
             print(f"{key:16s} full path: oae {fp['oae_pool']['latency_us']:.1f} us cold, msda+oae "
                   f"{fp['msda_then_oae']['latency_us']:.1f} us cold, oae err {fp['oae_max_abs_err_vs_oracle_8_queries']:.1e} "
                   f"{'OK' if fp['within_tolerance'] else 'FAIL'}")
+            if "cpu_reference_oae" in fp:
+                co = fp["cpu_reference_oae"]
+                print(f"{key:16s} cpu reference oae {co['full_call_s'] * 1e3:.0f} ms, err {co['gpu_max_abs_err_on_sample']:.1e}")
         if "frame" in c:
             for p, v in c["frame"].items():
                 print(f"{key:16s} frame {p:8s} {v['frame_us']:8.1f} us  per layer {v['per_layer_us']:.1f}")
