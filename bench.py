@@ -803,7 +803,7 @@ def _cpu_ref_dense(table, tiles, shape, loc, w, oracle_out):
                for g in range(G)]
         return time.perf_counter() - t0, np.concatenate(res, axis=1)
 
-    run(max(2 * workers, Q // 50))  # warm-up: the reference's packed-pair caches of every grid
+    run(min(Q, max(2 * workers, Q // 50)))  # warm-up: the reference's packed-pair caches of every grid
     t, got = run(Q)  # the full call (a query subset would over-state it: the per-tile costs dominate small subsets)
     return {"full_call_s": t, "camera_frames_per_s": cams / t, "cores": workers, "kind": "reference",
             "sample": f"the full call: {Q} anchors x {G} channel-group calls, 1 rep after a warm-up",
