@@ -395,13 +395,27 @@ cudaError_t launch_dense_coarse(const msda_features_t& f, const DenseFastSpec& d
   a.out = out;
   a.wsum = wsum;
   a.n_slices = C / slice_elems;
-  // anchor chunks: ~7 waves of items over the SMs, chunks of >= 64 anchors
+  // anchor chunks: every warp of an item takes whole 8-anchor blocks, so a
+  // chunk is a multiple of kStWarps x 8 anchors (65-anchor chunks at cfg1 ran
+  // 9 blocks on 8 warps: a lone second round per item); among those, the
+  // fewest rounds of (block rounds per item + a staging) over the SMs
   const int64_t pairs = (int64_t)f.batch * f.n_cams * a.n_slices;
-  // (measured at cfg3: 7 waves 164 us; 2 / 4 / 10 / 14 waves 174-207 us; chunks
-  // of 128-900 anchors 173-188 us)
-  int n_chunks = (int)std::max<int64_t>(1, (7 * 148 + pairs / 2) / pairs);
-  n_chunks = std::min(n_chunks, std::max(1, d.Q / 64));
-  a.chunk = (d.Q + n_chunks - 1) / n_chunks;
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  constexpr int kBlockAnchors = kStWarps * 8;
+  double best = 1e30;
+  a.chunk = kBlockAnchors;
+  for (int c = kBlockAnchors;; c += kBlockAnchors) {
+    const int64_t items = pairs * ((d.Q + c - 1) / c);
+    // (staging weight 0.5 / 1 / 2 measured alike; 0.25 picks smaller chunks, cfg3 375 vs 369 us)
+    const double cost = (double)((items + sms - 1) / sms) * ((c / kBlockAnchors) + 0.5);
+    if (cost < best - 1e-9) {
+      best = cost;
+      a.chunk = c;
+    }
+    if (c >= d.Q) break;
+  }
   a.n_chunks = (d.Q + a.chunk - 1) / a.chunk;
   a.n_items = pairs * a.n_chunks;
   a.zero_off = kStageBudget;
