@@ -973,6 +973,7 @@ cudaError_t launch_gather_dense_fast(const msda_features_t& f, const DenseFastSp
         if (d.h2) return launch_gather_pipe<__half, 8, false, 4, true, 8, true, true>(g, stream);
         return launch_gather_pipe<__half, 8, false, 4, true, 8, true>(g, stream);
       case MSDA_BF16: return launch_gather_pipe<__nv_bfloat16, 8, false, 4, true, 8, true>(g, stream);
+      case MSDA_F32: return launch_gather_pipe<float, 4, false, 4, true, 8, true>(g, stream);
       default: return cudaErrorNotSupported;
     }
   }

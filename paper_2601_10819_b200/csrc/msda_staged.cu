@@ -328,11 +328,9 @@ cudaError_t launch_coarse_t(const CUtensorMap& map, const StagedArgs& a, size_t 
 }  // namespace
 
 int dense_staged_fine_levels(const msda_features_t& f, int G, int P) {
-  // 2-byte storage only: with f32 rows (1 KB) the anchor-major gather moves
-  // twice the bytes per instruction the 128-B staged slices do, and the split
-  // measured slower (cfg1 f32 108 vs 94 us)
-  if (f.dtype == MSDA_F32) return -1;
-  const int esz = 2;
+  // f32 too: 128-B slices of 32 channels (cfg1 f32 FAST 94 -> 86 us once the
+  // anchor chunks are whole warp blocks; it measured 108 us with ragged ones)
+  const int esz = f.dtype == MSDA_F32 ? 4 : 2;
   const int C = f.channels;
   if (f.n_levels != kMaxLevels || !f.spatial_shape_host || P < 1 || G < 1 || C % G ||
       (C * esz) % kSliceBytes || (C / G) % (32 / esz))
@@ -427,6 +425,7 @@ cudaError_t launch_dense_coarse(const msda_features_t& f, const DenseFastSpec& d
       return d.h2 ? launch_coarse_t<__half, true>(map, a, smem, stream)
                   : launch_coarse_t<__half, false>(map, a, smem, stream);
     case MSDA_BF16: return launch_coarse_t<__nv_bfloat16, false>(map, a, smem, stream);
+    case MSDA_F32: return launch_coarse_t<float, false>(map, a, smem, stream);
     default: return cudaErrorNotSupported;
   }
 }

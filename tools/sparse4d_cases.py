@@ -47,11 +47,11 @@ def make_dense_inputs(bs, Q, P, cams, L, G, dev, seed=1):
 
 def staged_fine_levels(levels, dtype):
     """The dense FAST split the library makes (csrc/msda_staged.cu
-    dense_staged_fine_levels): 2-byte storage, 4 levels, levels 2-3 of every
-    camera fit 120 KB as 128-B row slices padded to 64-row TMA boxes -> the
-    gather moves levels 0-1 from L2, levels 2-3 come from shared memory.
-    Returns 2, or None when the anchor-major gather takes every level."""
-    if torch.finfo(dtype).bits != 16 or len(levels) != 4:
+    dense_staged_fine_levels): 4 levels whose levels 2-3 of every camera fit
+    120 KB as 128-B row slices padded to 64-row TMA boxes -> the gather moves
+    levels 0-1 from L2, levels 2-3 come from shared memory (any storage
+    dtype).  Returns 2, or None when the anchor-major gather takes every level."""
+    if len(levels) != 4:
         return None
     stage = sum((h * w + 63) // 64 * 64 * 128 for h, w in levels[2:])
     return 2 if stage <= 120 * 1024 else None
