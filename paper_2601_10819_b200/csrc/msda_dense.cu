@@ -738,78 +738,64 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
   if (nq == 0) return MSDA_OK;
   if (precision == MSDA_FAST || precision == MSDA_FAST_H2) {
     const bool h2 = precision == MSDA_FAST_H2;
-    if (!project) {  // pipelined gather (msda_exact.cu); shapes it does not take use the warp-camera kernel
-      // the exact records' space is free in FAST: it holds the split weight sums
-      float* scratch = reinterpret_cast<float*>(ew.rec);
-      const DenseFastSpec d{loc, w, Q, P, G, normalize, wsum_out, scratch, h2};
-      bool pending = false;
-      cudaError_t e = cudaErrorNotSupported;
-      const int n_fine = dense_staged_fine_levels(*f, G, P);
-      if (n_fine > 0) {  // coarse levels from on-chip staged maps, fine levels by the pipelined gather
-        float* wsum = wsum_out ? wsum_out : (normalize ? scratch : nullptr);
-        e = cudaMemsetAsync(out, 0, (size_t)nq * a.C * 4, s);
-        if (e == cudaSuccess && wsum) e = cudaMemsetAsync(wsum, 0, (size_t)nq * G * 4, s);
-        // coarse levels (shared-memory-bound, no L2 gathers) on a forked
-        // high-priority stream beside the fine levels' gather (L2-bound):
-        // one 256-thread coarse CTA per SM, the gather's one-warp CTAs fill
-        // the rest; both red.add into the zeroed totals, the join orders
-        // them before whatever follows on s (capturable in a CUDA graph)
-        const AuxStream& x = aux_stream();
-        if (e == cudaSuccess && x.ok) {
-          e = cudaEventRecord(x.fork, s);
-          if (e == cudaSuccess) e = cudaStreamWaitEvent(x.stream, x.fork, 0);
-          if (e == cudaSuccess) e = launch_dense_coarse(*f, d, n_fine, out, wsum, x.stream);
-          if (e == cudaSuccess) e = cudaEventRecord(x.join, x.stream);
-        } else if (e == cudaSuccess) {
-          e = launch_dense_coarse(*f, d, n_fine, out, wsum, s);
-        }
-        if (e == cudaSuccess) {
-          DenseFastSpec fine = d;
-          fine.n_lv = n_fine;
-          fine.accumulate = true;
-          e = launch_gather_dense_fast(*f, fine, ew.status, out, s, &pending);
-          if (e == cudaErrorNotSupported) return MSDA_CUDA_ERROR;  // the staged plan implies the gather fits
-        }
-        if (e == cudaSuccess && x.ok) e = cudaStreamWaitEvent(s, x.join, 0);
-        if (e != cudaSuccess) return MSDA_CUDA_ERROR;
-      } else {
-        e = launch_gather_dense_fast(*f, d, ew.status, out, s, &pending);
-      }
-      if (e == cudaSuccess) {
-        if (pending) {
-          const int64_t total = nq * a.C;
-          const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
-          group_normalize_kernel<<<blocks, 256, 0, s>>>(out, wsum_out ? wsum_out : scratch, nq, a.C, G, ew.status);
-          if (cudaGetLastError() != cudaSuccess) return MSDA_CUDA_ERROR;
-        }
-        return MSDA_OK;
-      }
-      if (e != cudaErrorNotSupported) return MSDA_CUDA_ERROR;
-    }
-    if (project) {  // projection pre-pass, then the pipelined gather on its pixel coordinates
+    // the exact records' space is free in FAST: it holds the split weight sums
+    float* scratch = reinterpret_cast<float*>(ew.rec);
+    DenseFastSpec d{loc, w, Q, P, G, normalize, wsum_out, scratch, h2};
+    if (project) {  // projection pre-pass (f64): per-level cells of every (anchor, keypoint, camera)
       float2* uv = reinterpret_cast<float2*>(ew.g_hi);  // the exact sort scratch (8 B per sample) is free in FAST
       const int64_t n = nq * P * a.cams;
       const int blocks = (int)std::min<int64_t>((n + 127) / 128, 148 * 32);
       project_prepass_kernel<<<blocks, 128, 0, s>>>(a, uv);
       if (cudaGetLastError() != cudaSuccess) return MSDA_CUDA_ERROR;
-      float* scratch = reinterpret_cast<float*>(ew.rec);
-      DenseFastSpec d{nullptr, w, Q, P, G, normalize, wsum_out, scratch, h2};
+      d.loc = nullptr;
       d.proj_cell = uv;
-      bool pending = false;
-      cudaError_t e = launch_gather_dense_fast(*f, d, ew.status, out, s, &pending);
-      if (e == cudaSuccess) {
-        if (pending) {
-          const int64_t total = nq * a.C;
-          const int nb = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
-          group_normalize_kernel<<<nb, 256, 0, s>>>(out, wsum_out ? wsum_out : scratch, nq, a.C, G, ew.status);
-          if (cudaGetLastError() != cudaSuccess) return MSDA_CUDA_ERROR;
-        }
-        return MSDA_OK;
-      }
-      if (e != cudaErrorNotSupported) return MSDA_CUDA_ERROR;
     }
-    const cudaError_t e =
-        project ? launch_dense_fast<true>(a, f->dtype, h2, s) : launch_dense_fast<false>(a, f->dtype, h2, s);
+    // pipelined gather (msda_exact.cu); shapes it does not take use the warp-camera kernel
+    bool pending = false;
+    cudaError_t e = cudaErrorNotSupported;
+    const int n_fine = dense_staged_fine_levels(*f, G, P);
+    if (n_fine > 0) {  // coarse levels from on-chip staged maps, fine levels by the pipelined gather
+      float* wsum = wsum_out ? wsum_out : (normalize ? scratch : nullptr);
+      e = cudaMemsetAsync(out, 0, (size_t)nq * a.C * 4, s);
+      if (e == cudaSuccess && wsum) e = cudaMemsetAsync(wsum, 0, (size_t)nq * G * 4, s);
+      // coarse levels (shared-memory-bound, no L2 gathers) on a forked
+      // high-priority stream beside the fine levels' gather (L2-bound):
+      // one 256-thread coarse CTA per SM, the gather's one-warp CTAs fill
+      // the rest; both red.add into the zeroed totals, the join orders
+      // them before whatever follows on s (capturable in a CUDA graph)
+      const AuxStream& x = aux_stream();
+      if (e == cudaSuccess && x.ok) {
+        e = cudaEventRecord(x.fork, s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(x.stream, x.fork, 0);
+        if (e == cudaSuccess) e = launch_dense_coarse(*f, d, n_fine, out, wsum, x.stream);
+        if (e == cudaSuccess) e = cudaEventRecord(x.join, x.stream);
+      } else if (e == cudaSuccess) {
+        e = launch_dense_coarse(*f, d, n_fine, out, wsum, s);
+      }
+      if (e == cudaSuccess) {
+        DenseFastSpec fine = d;
+        fine.n_lv = n_fine;
+        fine.accumulate = true;
+        e = launch_gather_dense_fast(*f, fine, ew.status, out, s, &pending);
+        if (e == cudaErrorNotSupported) return MSDA_CUDA_ERROR;  // the staged plan implies the gather fits
+      }
+      if (e == cudaSuccess && x.ok) e = cudaStreamWaitEvent(s, x.join, 0);
+      if (e != cudaSuccess) return MSDA_CUDA_ERROR;
+    } else {
+      e = launch_gather_dense_fast(*f, d, ew.status, out, s, &pending);
+    }
+    if (e == cudaSuccess) {
+      if (pending) {
+        const int64_t total = nq * a.C;
+        const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+        group_normalize_kernel<<<blocks, 256, 0, s>>>(out, wsum_out ? wsum_out : scratch, nq, a.C, G, ew.status);
+        if (cudaGetLastError() != cudaSuccess) return MSDA_CUDA_ERROR;
+      }
+      return MSDA_OK;
+    }
+    if (e != cudaErrorNotSupported) return MSDA_CUDA_ERROR;
+    // shapes the pipelined gather does not take: the warp-camera kernel (projecting itself)
+    e = project ? launch_dense_fast<true>(a, f->dtype, h2, s) : launch_dense_fast<false>(a, f->dtype, h2, s);
     return e == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
   }
   if (precision == MSDA_EXACT_HALF && f->dtype != MSDA_F16) return MSDA_BAD_ARG;

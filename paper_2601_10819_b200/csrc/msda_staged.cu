@@ -59,6 +59,7 @@ struct StagedArgs {
   const float* w;        // [bs, Q, P, cams, 4, G]
   float* out;            // [bs, Q, C], zeroed
   float* wsum;           // [bs, Q, G], zeroed, or null
+  const float2* proj_cell;  // fused projection: cells [bs, Q, P, cams, 4] (NaN: behind the camera), or null
   int32_t n_slices, n_chunks, chunk;  // slices per row, anchor chunks, anchors per chunk
   int64_t n_items;
   int32_t zero_off;  // byte offset of the 128-B zero row (the stage area [0, kStageBudget) precedes it)
@@ -179,12 +180,18 @@ __global__ void __launch_bounds__(kStThreads, 1)
       const bool valid = qi < n_anchor;
       const int64_t bq = (int64_t)b * a.Q + q0 + (valid ? qi : 0);
       const int64_t pc0 = bq * a.P * a.cams + cam;  // (bq, p = 0, cam); p adds a.cams
-      // locations / weights of keypoints p and p + 1 in flight (two buffers)
-      float2 bl[2];
+      // locations (or, fused projection, the pre-pass's cells of the coarse
+      // levels) and weights of keypoints p and p + 1 in flight (two buffers)
+      float2 bl[2][kCoarse];
       float bw[2][kCoarse];
       auto load_pt = [&](int p, int k2) {
         const int64_t pc = pc0 + (int64_t)min(p, a.P - 1) * a.cams;
-        bl[k2] = __ldg(reinterpret_cast<const float2*>(a.loc) + pc);
+        if (a.proj_cell) {
+#pragma unroll
+          for (int k = 0; k < kCoarse; ++k) bl[k2][k] = __ldg(a.proj_cell + pc * kMaxLevels + kFine + k);
+        } else {
+          bl[k2][0] = __ldg(reinterpret_cast<const float2*>(a.loc) + pc);
+        }
 #pragma unroll
         for (int k = 0; k < kCoarse; ++k) bw[k2][k] = __ldg(a.w + (pc * kMaxLevels + kFine + k) * a.G + g_lane);
       };
@@ -201,16 +208,27 @@ __global__ void __launch_bounds__(kStThreads, 1)
 #pragma unroll
         for (int k2 = 0; k2 < 2; ++k2) {
           if (p0 + k2 >= a.P) break;
-          const float2 lp = bl[k2];
+          float2 lp[kCoarse];
           float wl[kCoarse];
 #pragma unroll
-          for (int k = 0; k < kCoarse; ++k) wl[k] = bw[k2][k];
+          for (int k = 0; k < kCoarse; ++k) {
+            lp[k] = bl[k2][k];
+            wl[k] = bw[k2][k];
+          }
           load_pt(p0 + k2 + 2, k2);  // keypoint p + 2 into this buffer (clamped past P)
 #pragma unroll
           for (int l = kCoarse - 1; l >= 0; --l) {
             const int W = lW[l], H = lH[l];
-            const float u = __fsub_rn(__fmul_rn(lp.x, (float)W), 0.5f);
-            const float v = __fsub_rn(__fmul_rn(lp.y, (float)H), 0.5f);
+            float u, v, wg = wl[l];
+            if (a.proj_cell) {  // cell = f32(pixel / stride - 0.5) from the pre-pass; NaN: behind, out of the plan
+              const bool ok = !isnan(lp[l].x);
+              u = ok ? lp[l].x : -4.0f;
+              v = ok ? lp[l].y : -4.0f;
+              wg = ok ? wg : 0.0f;
+            } else {  // cell = loc * W - 0.5 (features.py:20-24)
+              u = __fsub_rn(__fmul_rn(lp[0].x, (float)W), 0.5f);
+              v = __fsub_rn(__fmul_rn(lp[0].y, (float)H), 0.5f);
+            }
             const float uc = fminf(fmaxf(u, -2.0f), (float)W + 1.0f);  // keeps the integer conversion in range
             const float vc = fminf(fmaxf(v, -2.0f), (float)H + 1.0f);
             const float x0f = floorf(uc), y0f = floorf(vc);
@@ -222,7 +240,6 @@ __global__ void __launch_bounds__(kStThreads, 1)
             const uint32_t addr[4] = {vx0 && vy0 ? rb : zero_row, vx1 && vy0 ? rb + kSliceBytes : zero_row,
                                       vx0 && vy1 ? rb + W * kSliceBytes : zero_row,
                                       vx1 && vy1 ? rb + (W + 1) * kSliceBytes : zero_row};
-            const float wg = wl[l];
             const float omu = 1.0f - fu, omv = 1.0f - fv;
             const float c[4] = {omu * omv * wg, fu * omv * wg, omu * fv * wg, fu * fv * wg};
             wacc += wg;
@@ -335,6 +352,8 @@ int dense_staged_fine_levels(const msda_features_t& f, int G, int P) {
   if (f.n_levels != kMaxLevels || !f.spatial_shape_host || P < 1 || G < 1 || C % G ||
       (C * esz) % kSliceBytes || (C / G) % (32 / esz))
     return -1;
+  // the fine levels' gather takes whole 16-B-lane warps over a row, each lane in one group
+  if (C % (32 * (16 / esz)) || (C / G) % (16 / esz)) return -1;
   if (reinterpret_cast<uintptr_t>(f.data) % 16 || (int64_t)f.batch * f.n_rows >= (int64_t(1) << 31)) return -1;
   if (!encode_fn()) return -1;
   // the coarsest levels whose 128-B row slices (padded to whole TMA boxes)
@@ -390,6 +409,7 @@ cudaError_t launch_dense_coarse(const msda_features_t& f, const DenseFastSpec& d
   a.start = f.scale_start_index;
   a.loc = d.loc;
   a.w = d.w;
+  a.proj_cell = d.proj_cell;
   a.out = out;
   a.wsum = wsum;
   a.n_slices = C / slice_elems;
