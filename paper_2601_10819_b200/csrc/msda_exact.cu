@@ -941,10 +941,18 @@ cudaError_t launch_gather_dense_fast(const msda_features_t& f, const DenseFastSp
   g.n_lv = d.n_lv > 0 ? std::min(d.n_lv, f.n_levels) : f.n_levels;
   g.accumulate = d.accumulate ? 1 : 0;
   const int per_cam = d.P * g.n_lv;
-  // fine levels beside the staged kernel: chains of 52 samples (2 cameras at
-  // the cfg1 shape) — measured 26 / 52 / 104 / 156: cfg3 FAST_H2 371 / 365 /
-  // 369 / — us, cfg4 FAST 221 / 222 / 229 us, cfg1 f16 FAST_H2 51 / 53 / 57 / 60 us
-  const int split_samples = d.accumulate ? kDenseSplitSamples / 4 : kDenseSplitSamples;
+  // fine levels beside the staged kernel: chains of 104 samples, halved
+  // (down to 26) while the grid has fewer than ~20 k warps — small calls are
+  // latency-bound and want more, shorter chains; large batches pay for the
+  // extra partial red.adds.  Measured 26 / 52 / 104 / 156: cfg3 FAST_H2
+  // 371 / 365 / 369 / — us, cfg4 FAST 221 / 222 / 229 us, cfg1 f16 FAST_H2
+  // 51 / 53 / 57 / 60 us; cfg5-stream (16 scenes x 32 cameras) 3.68 ms at 52
+  // vs 3.58 ms at 104
+  int split_samples = d.accumulate ? kDenseSplitSamples / 2 : kDenseSplitSamples;
+  if (d.accumulate)
+    while (split_samples > kDenseSplitSamples / 8 &&
+           g.n_queries * ((f.n_cams * per_cam + split_samples - 1) / split_samples) < 20000)
+      split_samples /= 2;
   const int want = std::max(1, (f.n_cams * per_cam + split_samples - 1) / split_samples);
   g.cps = (f.n_cams + want - 1) / want;
   g.n_split = (f.n_cams + g.cps - 1) / g.cps;
@@ -965,7 +973,7 @@ cudaError_t launch_gather_dense_fast(const msda_features_t& f, const DenseFastSp
   if (d.accumulate) {
     // fine levels only (the coarse ones come from the staged kernel): every
     // corner row is an L2 miss or a far L2 hit, so a deeper ring (4 samples
-    // in flight per warp) and shorter chains (52 samples per warp, above) win —
+    // in flight per warp) and shorter chains (26-104 samples per warp, above) win —
     // cfg3 FAST_H2 fine part 227 vs 300 us (D = 2, 208), measured D in
     // {2, 3, 4, 6, 8} x chains {26, 52, 104, 156, 208, 416}
     switch (f.dtype) {

@@ -100,7 +100,7 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
 // work per sample is shared by 4 lanes, not 8.  The two chunk loads of odd
 // groups are issued in swapped order, which keeps every quarter-warp phase of
 // an LDS.128 on 32 distinct banks.
-template <typename T, bool HACC>
+template <typename T, bool HACC, bool PROJ>
 __global__ void __launch_bounds__(kStThreads, 1)
     staged_coarse_kernel(const __grid_constant__ CUtensorMap tmap, const StagedArgs a) {
   constexpr int LB = 32;                               // bytes per lane
@@ -182,11 +182,11 @@ __global__ void __launch_bounds__(kStThreads, 1)
       const int64_t pc0 = bq * a.P * a.cams + cam;  // (bq, p = 0, cam); p adds a.cams
       // locations (or, fused projection, the pre-pass's cells of the coarse
       // levels) and weights of keypoints p and p + 1 in flight (two buffers)
-      float2 bl[2][kCoarse];
+      float2 bl[2][PROJ ? kCoarse : 1];
       float bw[2][kCoarse];
       auto load_pt = [&](int p, int k2) {
         const int64_t pc = pc0 + (int64_t)min(p, a.P - 1) * a.cams;
-        if (a.proj_cell) {
+        if constexpr (PROJ) {
 #pragma unroll
           for (int k = 0; k < kCoarse; ++k) bl[k2][k] = __ldg(a.proj_cell + pc * kMaxLevels + kFine + k);
         } else {
@@ -208,19 +208,18 @@ __global__ void __launch_bounds__(kStThreads, 1)
 #pragma unroll
         for (int k2 = 0; k2 < 2; ++k2) {
           if (p0 + k2 >= a.P) break;
-          float2 lp[kCoarse];
+          float2 lp[PROJ ? kCoarse : 1];
           float wl[kCoarse];
 #pragma unroll
-          for (int k = 0; k < kCoarse; ++k) {
-            lp[k] = bl[k2][k];
-            wl[k] = bw[k2][k];
-          }
+          for (int k = 0; k < (PROJ ? kCoarse : 1); ++k) lp[k] = bl[k2][k];
+#pragma unroll
+          for (int k = 0; k < kCoarse; ++k) wl[k] = bw[k2][k];
           load_pt(p0 + k2 + 2, k2);  // keypoint p + 2 into this buffer (clamped past P)
 #pragma unroll
           for (int l = kCoarse - 1; l >= 0; --l) {
             const int W = lW[l], H = lH[l];
             float u, v, wg = wl[l];
-            if (a.proj_cell) {  // cell = f32(pixel / stride - 0.5) from the pre-pass; NaN: behind, out of the plan
+            if constexpr (PROJ) {  // cell = f32(pixel / stride - 0.5) from the pre-pass; NaN: behind, out of the plan
               const bool ok = !isnan(lp[l].x);
               u = ok ? lp[l].x : -4.0f;
               v = ok ? lp[l].y : -4.0f;
@@ -324,22 +323,27 @@ EncodeTiled encode_fn() {
   return fn;
 }
 
-template <typename T, bool HACC>
-cudaError_t launch_coarse_t(const CUtensorMap& map, const StagedArgs& a, size_t smem, cudaStream_t s) {
+template <typename T, bool HACC, bool PROJ>
+cudaError_t launch_coarse_p(const CUtensorMap& map, const StagedArgs& a, size_t smem, cudaStream_t s) {
   static std::atomic<bool> attr[64];
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || !attr[dev].load(std::memory_order_acquire)) {
     const cudaError_t e =
-        cudaFuncSetAttribute(staged_coarse_kernel<T, HACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(staged_coarse_kernel<T, HACC, PROJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) attr[dev].store(true, std::memory_order_release);
   }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t grid = std::min<int64_t>(a.n_items, sms);
-  staged_coarse_kernel<T, HACC><<<(unsigned)grid, kStThreads, smem, s>>>(map, a);
+  staged_coarse_kernel<T, HACC, PROJ><<<(unsigned)grid, kStThreads, smem, s>>>(map, a);
   return cudaGetLastError();
+}
+
+template <typename T, bool HACC>
+cudaError_t launch_coarse_t(const CUtensorMap& map, const StagedArgs& a, size_t smem, cudaStream_t s) {
+  return a.proj_cell ? launch_coarse_p<T, HACC, true>(map, a, smem, s) : launch_coarse_p<T, HACC, false>(map, a, smem, s);
 }
 
 }  // namespace
