@@ -399,7 +399,7 @@ def test_dense_zero_weight_sum_raises(cuda_dev, cams, precision):
 
 
 @pytest.mark.parametrize("cams,levels,dt", [
-    (6, [(64, 176), (32, 88), (16, 44), (8, 22)], "float32"),      # cfg1: 2 camera groups
+    (6, [(64, 176), (32, 88), (16, 44), (8, 22)], "float32"),      # cfg1 (f32 staged coarse levels)
     (16, [(270, 480), (135, 240), (68, 120), (34, 60)], "float32"),  # cfg2 shape: 4 camera groups, maps >> L2
     (32, [(64, 176), (32, 88), (16, 44), (8, 22)], "bfloat16"),    # cfg4 MSDA part (staged coarse levels)
     (64, [(64, 176), (32, 88), (16, 44), (8, 22)], "float16")])    # cfg3 per layer (staged coarse levels)
