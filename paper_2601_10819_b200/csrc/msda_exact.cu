@@ -972,16 +972,18 @@ cudaError_t launch_gather_dense_fast(const msda_features_t& f, const DenseFastSp
   // cfg1-cfg4, D in {2, 3, 4, 5, 7} x split in {104, 156, 208, 416} samples
   if (d.accumulate) {
     // fine levels only (the coarse ones come from the staged kernel): every
-    // corner row is an L2 miss or a far L2 hit, so a deeper ring (4 samples
-    // in flight per warp) and shorter chains (26-104 samples per warp, above) win —
-    // cfg3 FAST_H2 fine part 227 vs 300 us (D = 2, 208), measured D in
-    // {2, 3, 4, 6, 8} x chains {26, 52, 104, 156, 208, 416}
+    // corner row is an L2 miss or a far L2 hit, so a deeper ring than the
+    // all-level gather's and shorter chains (26-104 samples per warp, above)
+    // win — cfg3 FAST_H2 fine part 227 vs 300 us (D = 2, 208 then).  With the
+    // adaptive chains, D = 2 / 3 / 4 / 5 / 6: cfg3 FAST_H2 371 / 363 / 365 /
+    // 369 / 387 us, cfg3 FAST 456 / 463 / 467 / 475 / 498 us, cfg4 FAST 217 /
+    // 217 / 219 / 221 / 234 us
     switch (f.dtype) {
       case MSDA_F16:
-        if (d.h2) return launch_gather_pipe<__half, 8, false, 4, true, 8, true, true>(g, stream);
-        return launch_gather_pipe<__half, 8, false, 4, true, 8, true>(g, stream);
-      case MSDA_BF16: return launch_gather_pipe<__nv_bfloat16, 8, false, 4, true, 8, true>(g, stream);
-      case MSDA_F32: return launch_gather_pipe<float, 4, false, 4, true, 8, true>(g, stream);
+        if (d.h2) return launch_gather_pipe<__half, 8, false, 3, true, 8, true, true>(g, stream);
+        return launch_gather_pipe<__half, 8, false, 3, true, 8, true>(g, stream);
+      case MSDA_BF16: return launch_gather_pipe<__nv_bfloat16, 8, false, 3, true, 8, true>(g, stream);
+      case MSDA_F32: return launch_gather_pipe<float, 4, false, 3, true, 8, true>(g, stream);
       default: return cudaErrorNotSupported;
     }
   }
