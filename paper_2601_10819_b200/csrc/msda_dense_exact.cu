@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(32) dense_exact_kernel(const DenseExactArgs a)
   static_assert(BYTES == 16 || BYTES == 8, "8- or 16-B lanes");  // (8-B lanes, two warps per query: 1268 vs 957 us at cfg3)
   using SM = DxSmem<BYTES, D>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  static_assert((D & (D - 1)) == 0, "ring depth: a power of two");
   const int NB = a.ncs_pad;  // samples per camera buffer
   const int lane = threadIdx.x;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_raw);
@@ -197,7 +198,6 @@ __global__ void __launch_bounds__(32) dense_exact_kernel(const DenseExactArgs a)
   float acc[VEC];
 #pragma unroll
   for (int e = 0; e < VEC; ++e) acc[e] = 0.0f;
-  static_assert((D & (D - 1)) == 0, "ring depth: a power of two");
   uint32_t g = 0;  // global sample index; ring slot = g % D
   // one sample: its exact tree (products, sums, weight) — independent of acc
   auto tree = [&](int idx, uint32_t slot, float (&tw)[VEC]) {
@@ -233,6 +233,45 @@ __global__ void __launch_bounds__(32) dense_exact_kernel(const DenseExactArgs a)
       tw[e + 1] = r.y;
     }
   };
+  // N samples' trees interleaved channel pair by channel pair: all 4 N
+  // corner loads first, then for each pair the N samples' products and
+  // sums side by side (independent chains in program order), so the
+  // scheduler can cover FFMA2 / conversion latency with one warp per query
+  auto treeN = [&](auto nsm, int idx0, uint32_t g0, float (&tw)[decltype(nsm)::value][VEC]) {
+    constexpr int NS = decltype(nsm)::value;
+    uint4 iwr[NS];
+    float wn[NS];
+    RawVec<BYTES> cv[NS][4];
+#pragma unroll
+    for (int sm = 0; sm < NS; ++sm) {
+      iwr[sm] = *reinterpret_cast<const uint4*>(iw_w + idx0 + sm);
+      wn[sm] = wn_w[(idx0 + sm) * kGW + gl];
+      const uint32_t slot = (g0 + sm) % D;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) cv[sm][k] = *reinterpret_cast<const RawVec<BYTES>*>(ring_ptr + slot * SM::kSlot + k * 32 * BYTES);
+    }
+#pragma unroll
+    for (int e = 0; e < VEC; e += 2) {
+#pragma unroll
+      for (int sm = 0; sm < NS; ++sm) {
+        float2 c[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          float f[VEC];
+          to_f32<T, VEC>(cv[sm][k], f);
+          c[k] = make_float2(f[e], f[e + 1]);
+        }
+        const float2 p0 = __ffma2_rn(c[0], make_float2(__uint_as_float(iwr[sm].x), __uint_as_float(iwr[sm].x)), a.nz2);
+        const float2 p1 = __ffma2_rn(c[1], make_float2(__uint_as_float(iwr[sm].y), __uint_as_float(iwr[sm].y)), a.nz2);
+        const float2 p2 = __ffma2_rn(c[2], make_float2(__uint_as_float(iwr[sm].z), __uint_as_float(iwr[sm].z)), a.nz2);
+        const float2 p3 = __ffma2_rn(c[3], make_float2(__uint_as_float(iwr[sm].w), __uint_as_float(iwr[sm].w)), a.nz2);
+        const float2 t = __ffma2_rn(__ffma2_rn(p0, a.one2, p1), a.one2, __ffma2_rn(p2, a.one2, p3));
+        const float2 r = __ffma2_rn(t, make_float2(wn[sm], wn[sm]), a.nz2);
+        tw[sm][e] = r.x;
+        tw[sm][e + 1] = r.y;
+      }
+    }
+  };
   auto add = [&](const float (&tw)[VEC]) {  // acc + tw: the sequential sum (features.py:271-274)
 #pragma unroll
     for (int e = 0; e < VEC; e += 2) {
@@ -259,15 +298,12 @@ __global__ void __launch_bounds__(32) dense_exact_kernel(const DenseExactArgs a)
     if constexpr (D >= 8) {  // four samples per step: their trees overlap, the adds stay in order
       for (; j + 3 < n_cs; j += 4, g += 4) {
         cp_async_wait<D - 4>();
-        float t0[VEC], t1[VEC], t2[VEC], t3[VEC];
-        tree(buf + j, g % D, t0);
-        tree(buf + j + 1, (g + 1) % D, t1);
-        tree(buf + j + 2, (g + 2) % D, t2);
-        tree(buf + j + 3, (g + 3) % D, t3);
-        add(t0);
-        add(t1);
-        add(t2);
-        add(t3);
+        float tt[4][VEC];
+        treeN(std::integral_constant<int, 4>{}, buf + j, g, tt);
+        add(tt[0]);
+        add(tt[1]);
+        add(tt[2]);
+        add(tt[3]);
         refill(j, g % D);
         refill(j + 1, (g + 1) % D);
         refill(j + 2, (g + 2) % D);
@@ -276,11 +312,10 @@ __global__ void __launch_bounds__(32) dense_exact_kernel(const DenseExactArgs a)
     }
     for (; j + 1 < n_cs; j += 2, g += 2) {  // two samples: their trees overlap, the adds stay in order
       cp_async_wait<D - 2>();
-      float t0[VEC], t1[VEC];
-      tree(buf + j, g % D, t0);
-      tree(buf + j + 1, (g + 1) % D, t1);
-      add(t0);
-      add(t1);
+      float tt[2][VEC];
+      treeN(std::integral_constant<int, 2>{}, buf + j, g, tt);
+      add(tt[0]);
+      add(tt[1]);
       refill(j, g % D);
       refill(j + 1, (g + 1) % D);
     }
