@@ -251,6 +251,39 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // ---- the reference's exact f32 expression tree ----
+// Two samples' trees side by side (independent chains in program order), then
+// the two sequential adds: acc = (acc + t0) + t1, each rounded once — the same
+// bits as two exact_accumulate calls, with more instruction-level parallelism.
+template <int VEC>
+__device__ __forceinline__ void exact_accumulate2(float* acc, const float (*c0)[VEC], const float4 iw0, const float wn0,
+                                                  const float (*c1)[VEC], const float4 iw1, const float wn1, bool two,
+                                                  const float2 one2, const float2 nz2) {
+  static_assert(VEC % 2 == 0, "pairs");
+  float2 tw0[VEC / 2], tw1[VEC / 2];
+#pragma unroll
+  for (int e = 0; e < VEC; e += 2) {
+    const float2 a0 = __ffma2_rn(make_float2(c0[0][e], c0[0][e + 1]), make_float2(iw0.x, iw0.x), nz2);
+    const float2 a1 = __ffma2_rn(make_float2(c1[0][e], c1[0][e + 1]), make_float2(iw1.x, iw1.x), nz2);
+    const float2 b0 = __ffma2_rn(make_float2(c0[1][e], c0[1][e + 1]), make_float2(iw0.y, iw0.y), nz2);
+    const float2 b1 = __ffma2_rn(make_float2(c1[1][e], c1[1][e + 1]), make_float2(iw1.y, iw1.y), nz2);
+    const float2 d0 = __ffma2_rn(make_float2(c0[2][e], c0[2][e + 1]), make_float2(iw0.z, iw0.z), nz2);
+    const float2 d1 = __ffma2_rn(make_float2(c1[2][e], c1[2][e + 1]), make_float2(iw1.z, iw1.z), nz2);
+    const float2 f0 = __ffma2_rn(make_float2(c0[3][e], c0[3][e + 1]), make_float2(iw0.w, iw0.w), nz2);
+    const float2 f1 = __ffma2_rn(make_float2(c1[3][e], c1[3][e + 1]), make_float2(iw1.w, iw1.w), nz2);
+    const float2 t0 = __ffma2_rn(__ffma2_rn(a0, one2, b0), one2, __ffma2_rn(d0, one2, f0));
+    const float2 t1 = __ffma2_rn(__ffma2_rn(a1, one2, b1), one2, __ffma2_rn(d1, one2, f1));
+    tw0[e / 2] = __ffma2_rn(t0, make_float2(wn0, wn0), nz2);
+    tw1[e / 2] = __ffma2_rn(t1, make_float2(wn1, wn1), nz2);
+  }
+#pragma unroll
+  for (int e = 0; e < VEC; e += 2) {
+    float2 r = __ffma2_rn(tw0[e / 2], one2, make_float2(acc[e], acc[e + 1]));
+    if (two) r = __ffma2_rn(tw1[e / 2], one2, r);
+    acc[e] = r.x;
+    acc[e + 1] = r.y;
+  }
+}
+
 // acc[e] += wn * ((c0*w0 + c1*w1) + (c2*w2 + c3*w3)), two channels per FFMA2,
 // every product and sum rounded once (x*y + -0 == round(x*y); x*1 + y ==
 // round(x + y)).

@@ -731,8 +731,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
         if (two) fast_accumulate<VEC>(accf, c1, iw1, wn1);
         if constexpr (DENSE) wsum_g += two ? wn0 + wn1 : wn0;
       } else {
-        exact_accumulate<VEC>(accf, c0, iw0, wn0, a.one2, a.nz2);
-        if (two) exact_accumulate<VEC>(accf, c1, iw1, wn1, a.one2, a.nz2);
+        exact_accumulate2<VEC>(accf, c0, iw0, wn0, c1, iw1, wn1, two, a.one2, a.nz2);
       }
     } else {
       const void* p0[4] = {&cv0[0], &cv0[1], &cv0[2], &cv0[3]};
