@@ -51,21 +51,23 @@ def l2_ceiling():
 
 
 def time_fn(fn, reps, flush):
+    """Per-call CUDA-event times (ms), enqueued back to back without host
+    synchronisation (as bench.py's sparse4d block): a host sync per call would
+    add the host launch latency (~35 us per split dense call) to the device
+    time.  ``flush`` rewrites a 2x-L2 buffer before every call (cold)."""
     scratch = torch.empty(2 * L2 // 4, device="cuda") if flush else None
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
-    ts = []
-    for _ in range(reps):
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in ev:
         if flush:
             scratch.zero_()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         fn()
         b.record()
-        torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
-    ts.sort()
+    torch.cuda.synchronize()
+    ts = sorted(a.elapsed_time(b) for a, b in ev)
     return ts[len(ts) // 2], ts[0]
 
 
