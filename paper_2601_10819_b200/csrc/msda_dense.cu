@@ -600,7 +600,14 @@ cudaError_t launch_dense_offsets(int64_t* off, int64_t nq, int n, cudaStream_t s
 // it (geometry.py:162-182, f64) and writes every level's cell coordinate
 // cell[((bq * P + p) * cams + cam) * L + l] = f32(pixel / stride_l - 0.5)
 // (features.py:45-47), or NaN when depth <= 1e-6 (the sample leaves the plan).
-__global__ void project_prepass_kernel(DenseArgs a, float2* cell) {
+// (optionally also zeroing the split call's totals: out as float4 and the
+// weight sums, saving the memset launches in front of the split)
+__global__ void project_prepass_kernel(DenseArgs a, float2* cell, float4* zero4, int64_t n_zero4, float* zero1,
+                                       int64_t n_zero1) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_zero4; i += (int64_t)gridDim.x * blockDim.x)
+    zero4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_zero1; i += (int64_t)gridDim.x * blockDim.x)
+    zero1[i] = 0.0f;
   const int64_t n = (int64_t)a.bs * a.Q * a.P * a.cams;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int cam = (int)(i % a.cams);
@@ -741,11 +748,15 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
     // the exact records' space is free in FAST: it holds the split weight sums
     float* scratch = reinterpret_cast<float*>(ew.rec);
     DenseFastSpec d{loc, w, Q, P, G, normalize, wsum_out, scratch, h2};
+    const int n_fine = dense_staged_fine_levels(*f, G, P);
+    float* wsum = wsum_out ? wsum_out : (normalize ? scratch : nullptr);
+    const bool zeroed = project && n_fine > 0 && a.C % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0;
     if (project) {  // projection pre-pass (f64): per-level cells of every (anchor, keypoint, camera)
       float2* uv = reinterpret_cast<float2*>(ew.g_hi);  // the exact sort scratch (8 B per sample) is free in FAST
       const int64_t n = nq * P * a.cams;
       const int blocks = (int)std::min<int64_t>((n + 127) / 128, 148 * 32);
-      project_prepass_kernel<<<blocks, 128, 0, s>>>(a, uv);
+      project_prepass_kernel<<<blocks, 128, 0, s>>>(a, uv, reinterpret_cast<float4*>(out), zeroed ? nq * a.C / 4 : 0,
+                                                    wsum, (zeroed && wsum) ? nq * G : 0);
       if (cudaGetLastError() != cudaSuccess) return MSDA_CUDA_ERROR;
       d.loc = nullptr;
       d.proj_cell = uv;
@@ -753,11 +764,12 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
     // pipelined gather (msda_exact.cu); shapes it does not take use the warp-camera kernel
     bool pending = false;
     cudaError_t e = cudaErrorNotSupported;
-    const int n_fine = dense_staged_fine_levels(*f, G, P);
     if (n_fine > 0) {  // coarse levels from on-chip staged maps, fine levels by the pipelined gather
-      float* wsum = wsum_out ? wsum_out : (normalize ? scratch : nullptr);
-      e = cudaMemsetAsync(out, 0, (size_t)nq * a.C * 4, s);
-      if (e == cudaSuccess && wsum) e = cudaMemsetAsync(wsum, 0, (size_t)nq * G * 4, s);
+      e = cudaSuccess;
+      if (!zeroed) {
+        e = cudaMemsetAsync(out, 0, (size_t)nq * a.C * 4, s);
+        if (e == cudaSuccess && wsum) e = cudaMemsetAsync(wsum, 0, (size_t)nq * G * 4, s);
+      }
       // coarse levels (shared-memory-bound, no L2 gathers) on a forked
       // high-priority stream beside the fine levels' gather (L2-bound):
       // one 256-thread coarse CTA per SM, the gather's one-warp CTAs fill
