@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--json", default="")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU reference legs")
     args = ap.parse_args()
     import torch
 
