@@ -20,7 +20,7 @@ LIB = PKG / "lib" / "libmsda_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-warn-spills",
-         "-I", str(PKG.parent / "include")]
+         "-I", str(PKG.parent / "include"), *os.environ.get("MSDA_EXTRA_NVCC_FLAGS", "").split()]
 
 
 def sources():

@@ -43,6 +43,35 @@
 #include "msda_common.cuh"
 #include "msda_exact.cuh"
 
+#ifdef MSDA_PLAN_TL  // builder-only timeline (tools/plan_timeline.py): globaltimer stamps, never shipped
+__device__ unsigned long long g_msda_tl[8192][8];
+#define MSDA_TL(slot, k)                                                              \
+  do {                                                                                \
+    if ((threadIdx.x & 31) == 0 && (slot) < 8192) {                                   \
+      unsigned long long t_;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                        \
+      g_msda_tl[(slot)][(k)] = t_;                                                    \
+    }                                                                                 \
+  } while (0)
+#define MSDA_TL_SMID(slot)                                                            \
+  do {                                                                                \
+    uint32_t s_;                                                                      \
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(s_));                                  \
+    if ((threadIdx.x & 31) == 0 && (slot) < 8192) g_msda_tl[(slot)][3] = s_;          \
+  } while (0)
+extern "C" int msda_debug_timeline(void* host, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(host, g_msda_tl, bytes < sizeof(g_msda_tl) ? bytes : sizeof(g_msda_tl));
+}
+#else
+#define MSDA_TL(slot, k) \
+  do {                   \
+  } while (0)
+#define MSDA_TL_SMID(slot) \
+  do {                     \
+  } while (0)
+#endif
+#define MSDA_TL_WARP (2048 + (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)))
+
 namespace msda {
 
 namespace {
@@ -155,6 +184,7 @@ __global__ void __launch_bounds__(kPlanThreads, 7) plan_canon_kernel(PlanArgs a)
   // programmatic dependent launch: the gather grid may be scheduled now; it
   // waits (griddepcontrol.wait) for this grid's completion and memory flush
   asm volatile("griddepcontrol.launch_dependents;");
+  if (threadIdx.x == 0) MSDA_TL(blockIdx.x, 0);
 
   for (int64_t q = blockIdx.x; q < a.n_queries; q += gridDim.x) {
     const int64_t lo = a.offsets[q], hi = a.offsets[q + 1];
@@ -171,6 +201,7 @@ __global__ void __launch_bounds__(kPlanThreads, 7) plan_canon_kernel(PlanArgs a)
     else  // long query: global scratch (the wn slots double as its weight scratch)
       canon_query<false>(a, q, lo, n, n_tiles, a.g_hi + lo, a.g_lo + lo, a.wn + lo, s_run);
   }
+  if (threadIdx.x == 0) MSDA_TL(blockIdx.x, 5);
 }
 
 template <bool SMEM>
@@ -209,6 +240,7 @@ __device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_
       }
     }
     __syncthreads();
+    if (q == blockIdx.x && threadIdx.x == 0) MSDA_TL(blockIdx.x, 1);
     const int64_t row_base = (q / a.queries_per_batch) * a.rows_per_batch;
     // record + raw weight of the key at canonical slot `slot`
     auto emit = [&](u64 kt, u64 kp, int slot) {
@@ -233,6 +265,7 @@ __device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_
       }
     }
     bool rank_path = !__syncthreads_or(bad) && n_tiles <= kRunTable && n <= 32767;
+    if (q == blockIdx.x && threadIdx.x == 0) MSDA_TL(blockIdx.x, 2);
     if (rank_path) {  // canonical slot = run start + rank of (v, u) in the run
       bool long_run = false;
       for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -278,6 +311,7 @@ __device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_
       }
       rank_path = !__syncthreads_or(long_run);
     }
+    if (q == blockIdx.x && threadIdx.x == 0) MSDA_TL(blockIdx.x, 3);
     if (!rank_path) {  // ungrouped or long runs: full bitonic sort, slots = sorted order
       bitonic_sort_canon(khi, klo, n);
       for (int i = threadIdx.x; i < n; i += blockDim.x) emit(khi[i], klo[i], i);
@@ -288,6 +322,7 @@ __device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_
       if (ws == 0.0f) set_status(a.status, MSDA_ZERO_WEIGHT_SUM, q);
       a.qsum[q] = ws;
     }
+    if (q == blockIdx.x && threadIdx.x == 0) MSDA_TL(blockIdx.x, 4);
     __syncthreads();  // shared memory is reused by the next query
   }
 }
@@ -541,7 +576,9 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
   // launched programmatically after the canonicaliser: its records, weights
   // and sums are visible once the primary grid has completed (a no-op when
   // launched normally)
+  if constexpr (!DENSE && !RAW) MSDA_TL(MSDA_TL_WARP, 0);
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if constexpr (!DENSE && !RAW) MSDA_TL(MSDA_TL_WARP, 1);
   // malformed CSR offsets (reported by the plan kernel): the workspace
   // records are not all written, read none of them
   if (!RAW && a.status && *reinterpret_cast<volatile const int32_t*>(&a.status->code) == MSDA_BAD_ARG) return;
@@ -797,6 +834,10 @@ __global__ void __launch_bounds__(kPipeWarps * 32) gather_pipe_kernel(GatherArgs
     }
   }
   if (c0 == 0 && a.empty) a.empty[q] = (n == 0) ? 1 : 0;
+  if constexpr (!DENSE && !RAW) {
+    MSDA_TL(MSDA_TL_WARP, 2);
+    MSDA_TL_SMID(MSDA_TL_WARP);
+  }
 }
 
 template <typename T, int VEC, bool HALF, int D, bool RAW, int GW = 1, bool DENSE = false, bool HACC = false>
