@@ -36,6 +36,12 @@ def _stale(obj: Path, src: Path) -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> Path:
     OBJ.mkdir(parents=True, exist_ok=True)
+    # objects built with other flags (e.g. a builder-only MSDA_EXTRA_NVCC_FLAGS
+    # timeline build) are stale whatever their mtimes
+    stamp = OBJ / "flags.txt"
+    flags = " ".join([*ARCH, *FLAGS])
+    if not stamp.exists() or stamp.read_text() != flags:
+        force = True
     srcs = sources()
     objs = [OBJ / (s.stem + ".o") for s in srcs]
 
@@ -54,6 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if force or changed or not LIB.exists():
         cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart"]
         subprocess.run(cmd, check=True)
+    stamp.write_text(flags)
     return LIB
 
 
