@@ -627,6 +627,15 @@ __global__ void project_prepass_kernel(DenseArgs a, float2* cell, float4* zero4,
   }
 }
 
+// the split FAST call's one zeroing launch: status block, totals, weight sums
+// (instead of three memset nodes ahead of the two accumulating kernels)
+__global__ void zero_totals_kernel(DevStatus* st, float4* z4, int64_t n4, float* z1, int64_t n1) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  if (t == 0) *st = DevStatus{};
+  for (int64_t i = t; i < n4; i += stride) z4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t i = t; i < n1; i += stride) z1[i] = 0.0f;
+}
+
 // out[q, c] /= weight_sums[q, c / (C / G)] (camera-sharded partials after the all-reduce)
 __global__ void group_normalize_kernel(float* out, const float* wsum, int64_t n_q, int C, int G, DevStatus* st) {
   const int cpg = C / G;
@@ -741,16 +750,26 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
   if (ws_bytes < exact_workspace_bytes(nq, S) + dense_exact_extra_bytes(nq, S)) return MSDA_BAD_ARG;
   ExactWorkspace ew = carve_exact_workspace(ws, S);
   a.status = ew.status;
-  if (reset_exact_workspace(ew, s) != cudaSuccess) return MSDA_CUDA_ERROR;
+  const bool fast = precision == MSDA_FAST || precision == MSDA_FAST_H2;
+  const int n_fine = fast && nq > 0 ? dense_staged_fine_levels(*f, G, P) : -1;
+  const bool aligned_out = a.C % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0;
+  // the split's totals are zeroed by one kernel: the projection pre-pass, or
+  // (plain calls) zero_totals_kernel, which also resets the status block
+  const bool zeroed = n_fine > 0 && aligned_out;
+  if (!(zeroed && !project) && reset_exact_workspace(ew, s) != cudaSuccess) return MSDA_CUDA_ERROR;
   if (nq == 0) return MSDA_OK;
-  if (precision == MSDA_FAST || precision == MSDA_FAST_H2) {
+  if (fast) {
     const bool h2 = precision == MSDA_FAST_H2;
     // the exact records' space is free in FAST: it holds the split weight sums
     float* scratch = reinterpret_cast<float*>(ew.rec);
     DenseFastSpec d{loc, w, Q, P, G, normalize, wsum_out, scratch, h2};
-    const int n_fine = dense_staged_fine_levels(*f, G, P);
     float* wsum = wsum_out ? wsum_out : (normalize ? scratch : nullptr);
-    const bool zeroed = project && n_fine > 0 && a.C % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0;
+    if (zeroed && !project) {
+      const int blocks = (int)std::min<int64_t>((nq * a.C / 4 + 255) / 256, 148 * 4);
+      zero_totals_kernel<<<blocks, 256, 0, s>>>(ew.status, reinterpret_cast<float4*>(out), nq * a.C / 4, wsum,
+                                                wsum ? nq * G : 0);
+      if (cudaGetLastError() != cudaSuccess) return MSDA_CUDA_ERROR;
+    }
     if (project) {  // projection pre-pass (f64): per-level cells of every (anchor, keypoint, camera)
       float2* uv = reinterpret_cast<float2*>(ew.g_hi);  // the exact sort scratch (8 B per sample) is free in FAST
       const int64_t n = nq * P * a.cams;
