@@ -604,6 +604,19 @@ cudaError_t launch_dense_offsets(int64_t* off, int64_t nq, int n, cudaStream_t s
 // weight sums, saving the memset launches in front of the split)
 __global__ void project_prepass_kernel(DenseArgs a, float2* cell, float4* zero4, int64_t n_zero4, float* zero1,
                                        int64_t n_zero1) {
+  // the call's status reset and its keypoint-offset check, both by one thread
+  // (the check depends on the learned offsets only, geometry.py:241-244): no
+  // other thread of any kernel of the call reports before this grid completes
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *a.status = DevStatus{};
+    for (int p = 7; p < a.P; ++p) {
+      const float* o = a.offsets + (p - 7) * 3;
+      if (!(fabsf(o[0]) <= 1.0f && fabsf(o[1]) <= 1.0f && fabsf(o[2]) <= 1.0f)) {
+        set_status(a.status, MSDA_OFFSET_RANGE, p);
+        break;
+      }
+    }
+  }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_zero4; i += (int64_t)gridDim.x * blockDim.x)
     zero4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_zero1; i += (int64_t)gridDim.x * blockDim.x)
@@ -615,8 +628,7 @@ __global__ void project_prepass_kernel(DenseArgs a, float2* cell, float4* zero4,
     const int64_t bq = bqp / a.P;
     const int p = (int)(bqp - bq * a.P);
     double kp[3];
-    if (!anchor_keypoint(a.anchors + bq * 10, p, a.offsets, a.dt, kp) && cam == 0)
-      set_status(a.status, MSDA_OFFSET_RANGE, p);
+    anchor_keypoint(a.anchors + bq * 10, p, a.offsets, a.dt, kp);  // range reported above
     double u, v;
     const bool ok = project_point(a, cam, kp, u, v);
     for (int l = 0; l < a.L; ++l) {
@@ -756,7 +768,10 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
   // the split's totals are zeroed by one kernel: the projection pre-pass, or
   // (plain calls) zero_totals_kernel, which also resets the status block
   const bool zeroed = n_fine > 0 && aligned_out;
-  if (!(zeroed && !project) && reset_exact_workspace(ew, s) != cudaSuccess) return MSDA_CUDA_ERROR;
+  // the status block is reset by the first kernel of the call where one of
+  // ours comes first (projection pre-pass, zeroing kernel), else by a memset
+  const bool kernel_reset = fast && nq > 0 && (project || zeroed);
+  if (!kernel_reset && reset_exact_workspace(ew, s) != cudaSuccess) return MSDA_CUDA_ERROR;
   if (nq == 0) return MSDA_OK;
   if (fast) {
     const bool h2 = precision == MSDA_FAST_H2;

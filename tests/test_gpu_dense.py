@@ -162,6 +162,42 @@ def test_dense_project_matches_composed_oracle(cuda_dev, normalize, channels, gr
         assert rel(out, ref) <= 1e-4, prec
 
 
+@pytest.mark.parametrize("channels", [256, 64])
+def test_dense_project_offset_out_of_range(cuda_dev, channels):
+    """A learned offset component beyond [-1, 1] raises the reference's
+    OffsetOutOfRange (geometry.py:241-244) on every projected path (pre-pass +
+    staged split at C = 256, the fused kernel at C = 64; FAST and EXACT), and
+    the next valid call on the same workspace succeeds (its status reset)."""
+    import torch
+
+    from paper_2601_10819_b200 import errors, ops
+
+    rng = np.random.default_rng(56)
+    cams, n_levels, groups = 4, 4, 8
+    grids, shape = {}, np.zeros((cams, n_levels, 2), dtype=np.int32)
+    for c in range(cams):
+        for m, s in enumerate([4.0, 8.0, 16.0, 32.0]):
+            h, w = int(math.ceil(256 / s)), int(math.ceil(704 / s))
+            grids[(c, m)] = rng.uniform(-1, 1, (h, w, channels)).astype(np.float32)
+            shape[c, m] = (h, w)
+    feats, _, _ = _feats(ops, torch, grids, shape, cuda_dev)
+    K, R, T = _ring(cams)
+    anchors = np.zeros((1, 8, 10), dtype=np.float32)
+    anchors[0, :, 0:2] = rng.uniform(-4, 4, (8, 2))
+    anchors[0, :, 2:6] = (0.9, 0.6, 0.6, 1.8)
+    good = rng.uniform(-1, 1, (6, 3)).astype(np.float32)
+    bad = good.copy()
+    bad[4, 1] = 1.25
+    wts = torch.from_numpy(rng.uniform(0.01, 1.0, (1, 8, 13, cams, n_levels, groups)).astype(np.float32)).to(cuda_dev)
+    camd = ops.Cameras(K, R, T, device=cuda_dev)
+    an = torch.from_numpy(anchors).to(cuda_dev)
+    for prec in ("fast", "exact"):
+        with pytest.raises(errors.OffsetOutOfRange):
+            ops.msda_dense_project(feats, an, bad, camd, [4.0, 8.0, 16.0, 32.0], wts, precision=prec, check=True)
+        out = ops.msda_dense_project(feats, an, good, camd, [4.0, 8.0, 16.0, 32.0], wts, precision=prec, check=True)
+        assert torch.isfinite(out).all()
+
+
 def test_oae_pool_matches_reference_golden(golden, cuda_dev):
     import torch
 
