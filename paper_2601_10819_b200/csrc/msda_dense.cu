@@ -770,7 +770,8 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
   const bool zeroed = n_fine > 0 && aligned_out;
   // the status block is reset by the first kernel of the call where one of
   // ours comes first (projection pre-pass, zeroing kernel), else by a memset
-  const bool kernel_reset = fast && nq > 0 && (project || zeroed);
+  const bool fused_exact = precision == MSDA_EXACT && !normalize && !project;
+  const bool kernel_reset = nq > 0 && ((fast && (project || zeroed)) || fused_exact);
   if (!kernel_reset && reset_exact_workspace(ew, s) != cudaSuccess) return MSDA_CUDA_ERROR;
   if (nq == 0) return MSDA_OK;
   if (fast) {
@@ -846,9 +847,10 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
   }
   if (precision == MSDA_EXACT_HALF && f->dtype != MSDA_F16) return MSDA_BAD_ARG;
   if (precision == MSDA_EXACT && !normalize && !project) {  // one fused pass: runs ranked in the gather warp
-    const cudaError_t e = launch_dense_exact_fused(*f, loc, w, Q, P, G, out, s);
+    const cudaError_t e = launch_dense_exact_fused(*f, loc, w, Q, P, G, out, ew.status, s);
     if (e == cudaSuccess) return MSDA_OK;
     if (e != cudaErrorNotSupported) return MSDA_CUDA_ERROR;
+    if (reset_exact_workspace(ew, s) != cudaSuccess) return MSDA_CUDA_ERROR;  // the fallback's kernels report
   }
   {  // EXACT, one pass for every group (bit-identical to the per-group plans below)
     const int n = P * a.cams * a.L;

@@ -52,6 +52,7 @@ struct DenseExactArgs {
   int64_t n_queries;
   int32_t ncs_pad;   // staged samples per camera buffer (levels x keypoints, rounded up to 4)
   float2 one2, nz2;  // FFMA2 operands that make exact adds / products (parameters: never fused)
+  DevStatus* status;  // reset by the first thread (no kernel of this call reports into it)
 };
 
 // per-warp shared memory: the corner ring, then two camera buffers of
@@ -127,6 +128,7 @@ __device__ __forceinline__ void stage_run(const DenseExactArgs& a, int lane, boo
 
 template <typename T, int VEC, int D>
 __global__ void __launch_bounds__(32) dense_exact_kernel(const DenseExactArgs a) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a.status) *a.status = DevStatus{};
   constexpr int BYTES = VEC * (int)sizeof(T);
   static_assert(BYTES == 16 || BYTES == 8, "8- or 16-B lanes");  // (8-B lanes, two warps per query: 1268 vs 957 us at cfg3)
   using SM = DxSmem<BYTES, D>;
@@ -383,7 +385,7 @@ cudaError_t launch_dx_depth(const DenseExactArgs& a, cudaStream_t s) {
 }  // namespace
 
 cudaError_t launch_dense_exact_fused(const msda_features_t& f, const float* loc, const float* w, int Q, int P, int G,
-                                     float* out, cudaStream_t stream) {
+                                     float* out, DevStatus* status, cudaStream_t stream) {
   const int C = f.channels;
   const int esz = f.dtype == MSDA_F32 ? 4 : 2;
   if (G < 1 || G > kGW || C % G || P < 1 || P > kMaxRun || f.n_levels > kMaxLv || f.n_levels * P > kMaxCamRun)
@@ -412,6 +414,7 @@ cudaError_t launch_dense_exact_fused(const msda_features_t& f, const float* loc,
   a.one2 = make_float2(1.0f, 1.0f);
   a.nz2 = make_float2(-0.0f, -0.0f);
   a.ncs_pad = (f.n_levels * P + 3) / 4 * 4;
+  a.status = status;
   switch (f.dtype) {  // the ring stays within one camera ahead of the consumer (D < levels x keypoints)
     case MSDA_F32: return launch_dx_depth<float, 4>(a, stream);
     case MSDA_F16: return launch_dx_depth<__half, 8>(a, stream);

@@ -65,7 +65,8 @@ cudaError_t launch_dense_coarse(const msda_features_t& f, const DenseFastSpec& d
 // Dense EXACT without normalisation in one pass: the gather warp ranks each
 // (camera, level) run itself (msda_dense_exact.cu).  cudaErrorNotSupported
 // when the shape does not fit (the caller takes the two-pass path).
+// status: reset by the kernel (the call's only kernel; nothing reports into it)
 cudaError_t launch_dense_exact_fused(const msda_features_t& f, const float* loc, const float* w, int Q, int P, int G,
-                                     float* out, cudaStream_t stream);
+                                     float* out, DevStatus* status, cudaStream_t stream);
 
 }  // namespace msda
