@@ -765,9 +765,10 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
   const bool fast = precision == MSDA_FAST || precision == MSDA_FAST_H2;
   const int n_fine = fast && nq > 0 ? dense_staged_fine_levels(*f, G, P) : -1;
   const bool aligned_out = a.C % 4 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0;
-  // the split's totals are zeroed by one kernel: the projection pre-pass, or
-  // (plain calls) zero_totals_kernel, which also resets the status block
-  const bool zeroed = n_fine > 0 && aligned_out;
+  // FAST totals are zeroed by one kernel: the projection pre-pass, or (plain
+  // calls) zero_totals_kernel, which also resets the status block (a split
+  // over levels or cameras red.adds into them; an unsplit gather overwrites)
+  const bool zeroed = fast && nq > 0 && aligned_out;
   // the status block is reset by the first kernel of the call where one of
   // ours comes first (projection pre-pass, zeroing kernel), else by a memset
   const bool fused_exact = precision == MSDA_EXACT && !normalize && !project;
@@ -829,6 +830,7 @@ int32_t run_dense(const msda_features_t* f, int32_t Q, int32_t P, int32_t G, con
       if (e == cudaSuccess && x.ok) e = cudaStreamWaitEvent(s, x.join, 0);
       if (e != cudaSuccess) return MSDA_CUDA_ERROR;
     } else {
+      d.prezeroed = zeroed;
       e = launch_gather_dense_fast(*f, d, ew.status, out, s, &pending);
     }
     if (e == cudaSuccess) {

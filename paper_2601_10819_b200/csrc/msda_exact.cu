@@ -999,7 +999,7 @@ cudaError_t launch_gather_dense_fast(const msda_features_t& f, const DenseFastSp
   if (g.n_split > 1 || d.accumulate) {
     if (!d.wsum_out && d.normalize && !d.wsum_scratch) return cudaErrorNotSupported;
     if (!d.wsum_out && d.normalize) g.wsum_out = d.wsum_scratch;
-    if (!d.accumulate) {
+    if (!d.accumulate && !d.prezeroed) {
       if (cudaMemsetAsync(out, 0, (size_t)g.n_queries * C * 4, stream) != cudaSuccess) return cudaErrorUnknown;
       if (g.wsum_out && cudaMemsetAsync(g.wsum_out, 0, (size_t)g.n_queries * G * 4, stream) != cudaSuccess)
         return cudaErrorUnknown;

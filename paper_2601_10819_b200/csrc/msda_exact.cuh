@@ -46,6 +46,7 @@ struct DenseFastSpec {
   const float2* proj_cell = nullptr;  // fused projection: cells [batch * Q, P, cams, L] (NaN: behind), or null
   int32_t n_lv = 0;        // gather only levels [0, n_lv) (0: all)
   bool accumulate = false;  // out / wsum are zeroed by the caller: always red.add, the caller normalises
+  bool prezeroed = false;   // out / wsum already zeroed by the caller (a camera split needs no memsets)
 };
 // *normalize_pending: the cameras were split across warps and out holds
 // unnormalised sums; the caller divides by wsum (out or scratch) per group.
