@@ -215,9 +215,27 @@ __global__ void __launch_bounds__(kOaeWarps * 32, 2) oae_warp_kernel(OaeArgs a) 
   const char* zrow = reinterpret_cast<const char*>(g_oae_zero_row) + (size_t)c0 * sizeof(T);
   const int units16 = (int)(row_bytes >> 4);  // row_bytes % 16 == 0 (C = 32 * VEC, 16-B lanes)
 
-  for (int p = threadIdx.x; p < a.P; p += blockDim.x)
-    if (!anchor_keypoint(a.anchors + (int64_t)q * 10, p, a.offsets, 0.0f, s_kp + 3 * p))
-      set_status(a.status, MSDA_OFFSET_RANGE, p);
+  if constexpr (SPLIT) {
+    // split launch: nothing else of this grid reports (the finishing kernel
+    // reports after it), so the call's status reset and the offset check
+    // (offsets only, geometry.py:241-244) are one thread's
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      *a.status = DevStatus{};
+      for (int p = 7; p < a.P; ++p) {
+        const float* o = a.offsets + (p - 7) * 3;
+        if (!(fabsf(o[0]) <= 1.0f && fabsf(o[1]) <= 1.0f && fabsf(o[2]) <= 1.0f)) {
+          set_status(a.status, MSDA_OFFSET_RANGE, p);
+          break;
+        }
+      }
+    }
+    for (int p = threadIdx.x; p < a.P; p += blockDim.x)
+      anchor_keypoint(a.anchors + (int64_t)q * 10, p, a.offsets, 0.0f, s_kp + 3 * p);
+  } else {
+    for (int p = threadIdx.x; p < a.P; p += blockDim.x)
+      if (!anchor_keypoint(a.anchors + (int64_t)q * 10, p, a.offsets, 0.0f, s_kp + 3 * p))
+        set_status(a.status, MSDA_OFFSET_RANGE, p);
+  }
   __syncthreads();
 
   float2 d2[VEC / 2];
@@ -518,7 +536,6 @@ int32_t msda_oae_pool(const msda_features_t* f, int32_t n_queries, const float* 
   a.out = out;
   a.occluded = all_occluded;
   a.status = reinterpret_cast<DevStatus*>(workspace);
-  if (cudaMemsetAsync(workspace, 0, sizeof(DevStatus), s) != cudaSuccess) return MSDA_CUDA_ERROR;
   a.n_grp = 1;
   if (oae_groups(f->n_cams) > 1 && workspace_bytes >= msda_oae_workspace_size(n_queries, f->n_cams, f->channels)) {
     a.n_grp = (int32_t)oae_groups(f->n_cams);
@@ -534,6 +551,11 @@ int32_t msda_oae_pool(const msda_features_t* f, int32_t n_queries, const float* 
   // the warp kernel projects one keypoint per lane (32-bit ballot): P <= 32
   const bool recs_fit = a.P <= 32 && a.P * a.L <= kOaeMaxRecs && (double)f->n_rows * f->channels * (f->dtype == MSDA_F32 ? 4 : 2) <
                                                         (double)(1ll << 35);
+  // the split warp kernel resets the status itself (its first thread); every other launch after a memset
+  const bool warp_path = recs_fit && al16 && ((f->dtype == MSDA_F32 && (C == 256 || C == 128)) ||
+                                              (f->dtype != MSDA_F32 && C == 256));
+  if (!(warp_path && a.n_grp > 1 && a.Q > 0) && cudaMemsetAsync(workspace, 0, sizeof(DevStatus), s) != cudaSuccess)
+    return MSDA_CUDA_ERROR;
   if (recs_fit && al16 && f->dtype == MSDA_F32 && C == 256) return launch_oae_warp<float, 8>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
   if (recs_fit && al16 && f->dtype == MSDA_F32 && C == 128) return launch_oae_warp<float, 4>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;
   if (recs_fit && al16 && f->dtype == MSDA_F16 && C == 256) return launch_oae_warp<__half, 8>(a, s) == cudaSuccess ? MSDA_OK : MSDA_CUDA_ERROR;

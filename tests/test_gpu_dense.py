@@ -288,6 +288,44 @@ def test_oae_pool_production_kernel(cuda_dev, dt, cams):
         assert np.abs(emb[q] - ref).max() <= 1e-4, q
 
 
+@pytest.mark.parametrize("cams", [6, 17])
+def test_oae_pool_offset_out_of_range(cuda_dev, cams):
+    """An out-of-range learned offset raises OffsetOutOfRange (geometry.py:241-
+    244) from the warp kernel, single CTA per query (6 cameras) and split over
+    camera groups (17, where the kernel's first thread resets the status);
+    the next valid call on the same workspace succeeds."""
+    import torch
+
+    from paper_2601_10819_b200 import errors, ops
+
+    rng = np.random.default_rng(62)
+    n_levels, channels, strides = 4, 256, [4.0, 8.0, 16.0, 32.0]
+    grids, shape = {}, np.zeros((cams, n_levels, 2), dtype=np.int32)
+    for c in range(cams):
+        for m, s in enumerate(strides):
+            h, w = int(math.ceil(256 / s)), int(math.ceil(704 / s))
+            grids[(c, m)] = rng.uniform(-1, 1, (h, w, channels)).astype(np.float32)
+            shape[c, m] = (h, w)
+    feats, _, _ = _feats(ops, torch, grids, shape, cuda_dev, dtype=torch.bfloat16)
+    K, R, T = _ring(cams)
+    camd = ops.Cameras(K, R, T, device=cuda_dev)
+    q_n = 5
+    anchors = np.zeros((q_n, 10), dtype=np.float32)
+    anchors[:, 0:2] = rng.uniform(-4, 4, (q_n, 2))
+    anchors[:, 2:6] = (0.9, 0.6, 0.6, 1.8)
+    good = rng.uniform(-1, 1, (6, 3)).astype(np.float32)
+    bad = good.copy()
+    bad[2, 0] = -1.5
+    t = lambda a: torch.from_numpy(a).to(cuda_dev)  # noqa: E731
+    desc, vis = t(rng.standard_normal((q_n, channels)).astype(np.float32)), t(np.ones((q_n, cams), np.float32))
+    mem = rng.standard_normal((q_n, channels)).astype(np.float32)
+    mem = t(mem / np.linalg.norm(mem, axis=1, keepdims=True))
+    with pytest.raises(errors.OffsetOutOfRange):
+        ops.oae_pool(feats, t(anchors), bad, camd, strides, desc, vis, mem)
+    emb, _ = ops.oae_pool(feats, t(anchors), good, camd, strides, desc, vis, mem)
+    assert torch.isfinite(emb).all()
+
+
 def _uniform_grids(rng, cams, levels, channels):
     grids = {}
     shape = np.zeros((cams, len(levels), 2), dtype=np.int32)
