@@ -171,16 +171,46 @@ __device__ __forceinline__ float sequential_sum(const float* sw, int n, bool vec
   return ws;
 }
 
+constexpr int kTileTab = 256;  // tiles whose (first row, H, W) a plan CTA keeps in shared memory
+
+// per-CTA shared tables of the plan kernel beside the key arrays (dynamic
+// shared memory sized by the tile count: cfg2 23.5 KB per CTA)
+struct PlanShared {
+  int16_t* run;   // [2 n_run] (first, one past last) position of each tile's run; n_run = 0: no rank path
+  int16_t* slot;  // [kPlanSmemCap] rank path: the canonical slot of the key at each position
+  int32_t* tstart;  // [n_tab] tile table: first row (batch offset not included); n_tab = 0: read global
+  int2* thw;        // [n_tab] (H, W)
+  int n_run, n_tab;
+};
+
+__host__ __device__ constexpr size_t plan_smem_bytes(int n_tiles) {
+  return (size_t)kPlanSmemCap * (8 + 8 + 4 + 2) + (n_tiles <= kRunTable ? 4 * (size_t)n_tiles : 0) +
+         (n_tiles <= kTileTab ? 12 * (size_t)n_tiles : 0) + 16;
+}
+
 template <bool SMEM>
 __device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_t lo, int n, int n_tiles, u64* khi,
-                                            u64* klo, float* sw, int16_t* s_run);
+                                            u64* klo, float* sw, const PlanShared& sh);
 
 __global__ void __launch_bounds__(kPlanThreads, 7) plan_canon_kernel(PlanArgs a) {
-  __shared__ __align__(16) u64 s_hi[kPlanSmemCap];
-  __shared__ __align__(16) u64 s_lo[kPlanSmemCap];
-  __shared__ __align__(16) float s_w[kPlanSmemCap];
-  __shared__ int16_t s_run[2 * kRunTable];
+  extern __shared__ __align__(16) unsigned char plan_smem[];
   const int n_tiles = a.n_cams * a.n_levels;
+  u64* s_hi = reinterpret_cast<u64*>(plan_smem);
+  u64* s_lo = s_hi + kPlanSmemCap;
+  float* s_w = reinterpret_cast<float*>(s_lo + kPlanSmemCap);
+  PlanShared sh;
+  sh.slot = reinterpret_cast<int16_t*>(s_w + kPlanSmemCap);
+  sh.n_run = n_tiles <= kRunTable ? n_tiles : 0;
+  sh.n_tab = n_tiles <= kTileTab ? n_tiles : 0;
+  sh.run = sh.slot + kPlanSmemCap;
+  sh.thw = reinterpret_cast<int2*>(plan_smem + ((kPlanSmemCap * 22 + 4 * sh.n_run + 7) & ~7));
+  sh.tstart = reinterpret_cast<int32_t*>(sh.thw + sh.n_tab);
+  // the tile table, read by every record this CTA writes (made visible by the
+  // first query's post-load barrier)
+  for (int t = threadIdx.x; t < sh.n_tab; t += blockDim.x) {
+    sh.tstart[t] = (int32_t)a.start[t];
+    sh.thw[t] = make_int2(a.shape[2 * t], a.shape[2 * t + 1]);
+  }
   // programmatic dependent launch: the gather grid may be scheduled now; it
   // waits (griddepcontrol.wait) for this grid's completion and memory flush
   asm volatile("griddepcontrol.launch_dependents;");
@@ -197,16 +227,17 @@ __global__ void __launch_bounds__(kPlanThreads, 7) plan_canon_kernel(PlanArgs a)
     // two inlined copies so the shared-memory one compiles to LDS/STS (a
     // pointer chosen at run time between smem and global would be generic)
     if (n <= kPlanSmemCap)
-      canon_query<true>(a, q, lo, n, n_tiles, s_hi, s_lo, s_w, s_run);
+      canon_query<true>(a, q, lo, n, n_tiles, s_hi, s_lo, s_w, sh);
     else  // long query: global scratch (the wn slots double as its weight scratch)
-      canon_query<false>(a, q, lo, n, n_tiles, a.g_hi + lo, a.g_lo + lo, a.wn + lo, s_run);
+      canon_query<false>(a, q, lo, n, n_tiles, a.g_hi + lo, a.g_lo + lo, a.wn + lo, sh);
   }
   if (threadIdx.x == 0) MSDA_TL(blockIdx.x, 5);
 }
 
 template <bool SMEM>
 __device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_t lo, int n, int n_tiles, u64* khi,
-                                            u64* klo, float* sw, int16_t* s_run) {
+                                            u64* klo, float* sw, const PlanShared& sh) {
+  int16_t* s_run = sh.run;
   {
     constexpr int U = 4;  // samples per thread whose loads are in flight together
     for (int i0 = threadIdx.x; i0 < n; i0 += U * blockDim.x) {
@@ -243,12 +274,19 @@ __device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_
     if (q == blockIdx.x && threadIdx.x == 0) MSDA_TL(blockIdx.x, 1);
     const int64_t row_base = (q / a.queries_per_batch) * a.rows_per_batch;
     // record + raw weight of the key at canonical slot `slot`
-    auto emit = [&](u64 kt, u64 kp, int slot) {
+    auto record = [&](u64 kt, u64 kp) {
       const int t = (int)(kt >> 32);
       const float vv = unord_f32((uint32_t)(kp >> 32));
       const float uu = unord_f32((uint32_t)(kp & 0xffffffffu));
       const int tt = t < n_tiles ? t : 0;
-      a.rec[lo + slot] = make_record(uu, vv, row_base + a.start[tt], a.shape[2 * tt], a.shape[2 * tt + 1]);
+      if (sh.n_tab) {  // shared tile table: no dependent global load per record
+        const int2 hw = sh.thw[tt];
+        return make_record(uu, vv, row_base + sh.tstart[tt], hw.x, hw.y);
+      }
+      return make_record(uu, vv, row_base + a.start[tt], a.shape[2 * tt], a.shape[2 * tt + 1]);
+    };
+    auto emit = [&](u64 kt, u64 kp, int slot) {
+      a.rec[lo + slot] = record(kt, kp);
       a.wn[lo + slot] = key_weight(kt);
       sw[slot] = key_weight(kt);
     };
@@ -259,12 +297,12 @@ __device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_
       const uint32_t tp = i > 0 ? (uint32_t)(khi[i - 1] >> 32) : 0xffffffffu;
       const uint32_t tn = i + 1 < n ? (uint32_t)(khi[i + 1] >> 32) : 0xffffffffu;
       bad |= i > 0 && t < tp;
-      if (t < (uint32_t)kRunTable) {
+      if (t < (uint32_t)sh.n_run) {
         if (t != tp) s_run[2 * t] = (int16_t)i;
         if (t != tn) s_run[2 * t + 1] = (int16_t)(i + 1);
       }
     }
-    bool rank_path = !__syncthreads_or(bad) && n_tiles <= kRunTable && n <= 32767;
+    bool rank_path = !__syncthreads_or(bad) && sh.n_run > 0 && n <= 32767;
     if (q == blockIdx.x && threadIdx.x == 0) MSDA_TL(blockIdx.x, 2);
     if (rank_path) {  // canonical slot = run start + rank of (v, u) in the run
       bool long_run = false;
@@ -307,7 +345,12 @@ __device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_
             rank += (wj < wi || (wj == wi && j < i)) ? 1 : 0;
           }
         }
-        emit(it, ip, rs + rank);
+        if constexpr (SMEM) {  // records are written below, beside the weight sum
+          sh.slot[i] = (int16_t)(rs + rank);
+          sw[rs + rank] = key_weight(it);
+        } else {
+          emit(it, ip, rs + rank);
+        }
       }
       rank_path = !__syncthreads_or(long_run);
     }
@@ -317,7 +360,18 @@ __device__ __forceinline__ void canon_query(const PlanArgs& a, int64_t q, int64_
       for (int i = threadIdx.x; i < n; i += blockDim.x) emit(khi[i], klo[i], i);
       __syncthreads();
     }
-    if (threadIdx.x == 0 && a.normalize) {  // sequential f32 sum in canonical order (features.py:264-269)
+    // sequential f32 sum in canonical order (features.py:264-269) by one
+    // thread; on the shared-memory rank path warps 1.. write the records and
+    // raw weights meanwhile
+    if (SMEM && rank_path && threadIdx.x >= 32) {
+      for (int i = threadIdx.x - 32; i < n; i += blockDim.x - 32) {
+        const int slot = sh.slot[i];
+        const u64 kt = khi[i];
+        a.rec[lo + slot] = record(kt, klo[i]);
+        a.wn[lo + slot] = key_weight(kt);
+      }
+    }
+    if (threadIdx.x == 0 && a.normalize) {
       const float ws = sequential_sum(sw, n, SMEM);
       if (ws == 0.0f) set_status(a.status, MSDA_ZERO_WEIGHT_SUM, q);
       a.qsum[q] = ws;
@@ -1098,7 +1152,7 @@ cudaError_t launch_plan_canon(const msda_features_t& f, const msda_csr_plan_t& p
   a.status = w.status;
   // one CTA per query while they all fit on the device at once
   const int64_t grid = std::min<int64_t>(p.n_queries, (int64_t)num_sms * 8);
-  plan_canon_kernel<<<(unsigned)grid, kPlanThreads, 0, stream>>>(a);
+  plan_canon_kernel<<<(unsigned)grid, kPlanThreads, plan_smem_bytes(f.n_cams * f.n_levels), stream>>>(a);
   return cudaGetLastError();
 }
 
